@@ -1,0 +1,254 @@
+"""CPU oracle for SeqCDC boundary detection -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` legs may import this package.  The product path
+(``paper_2505_21194_b200``) never imports it and shares no code with it.
+
+Three independent CPU formulations of the same method (§3.1-3.4,
+P:145-231; §4):
+
+* ``chunk``        -- the literal byte-at-a-time C loop in ``seqcdc_oracle.c``
+                      (ctypes).  This is THE oracle; every GPU parity test
+                      compares against it.
+* ``chunk_py``     -- a pure-Python twin of the same literal loop, for tiny
+                      inputs (brute force).
+* ``chunk_query``  -- a structurally different numpy formulation (first
+                      qualifying run vs. the SkipTrigger-th opposing pair,
+                      "first set bit" / "n-th set bit"), used to
+                      cross-check the literal loop.
+
+The readings adopted where the paper is ambiguous are listed in DESIGN.md
+("Readings") and in the header of ``seqcdc_oracle.c``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "seqcdc_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+INCREASING = 0
+DECREASING = 1
+
+
+@dataclass(frozen=True)
+class Params:
+    """SeqCDC parameters (Table I; min/max P:378)."""
+
+    mode: int = INCREASING          # 0 Increasing, 1 Decreasing
+    seq_length: int = 5             # L, bytes in a qualifying run
+    skip_trigger: int = 50          # T, opposing pairs that trigger a skip
+    skip_size: int = 256            # S, bytes skipped; 0 disables skipping
+    min_size: int = 4096
+    max_size: int = 16384
+
+    def check(self) -> None:
+        if self.mode not in (0, 1):
+            raise ValueError("mode must be 0 (Increasing) or 1 (Decreasing)")
+        if self.seq_length < 2:
+            raise ValueError("seq_length must be >= 2")
+        if self.skip_trigger < 1:
+            raise ValueError("skip_trigger must be >= 1")
+        if self.min_size < self.seq_length:
+            raise ValueError("min_size must be >= seq_length")
+        if self.max_size < self.min_size:
+            raise ValueError("max_size must be >= min_size")
+
+
+def table1(avg_kib: int, mode: int = INCREASING) -> Params:
+    """Table I with min = avg/2, max = 2*avg (BASELINE.json configs)."""
+    L, T, S = {4: (5, 55, 256), 8: (5, 50, 256), 16: (5, 50, 512)}[avg_kib]
+    avg = avg_kib * 1024
+    return Params(mode, L, T, S, avg // 2, 2 * avg)
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle with plain gcc -O2 (no SIMD intrinsics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        u64, u32, p = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p
+        lib.oracle_chunk.restype = ctypes.c_int64
+        lib.oracle_chunk.argtypes = [p, u64, u32, u32, u32, u32, u64, u64, p, u64, p]
+        lib.oracle_next_cut.restype = u64
+        lib.oracle_next_cut.argtypes = [p, u64, u64, u32, u32, u32, u32, u64, u64, p]
+        lib.oracle_chunk_batch.restype = ctypes.c_int64
+        lib.oracle_chunk_batch.argtypes = [p, p, u32, u32, u32, u32, u32, u64, u64, p, u64, p]
+        _lib = lib
+    return _lib
+
+
+def _as_u8(data) -> np.ndarray:
+    if isinstance(data, (bytes, bytearray, memoryview)):
+        return np.frombuffer(bytes(data), dtype=np.uint8)
+    a = np.ascontiguousarray(np.asarray(data, dtype=np.uint8))
+    return a
+
+
+def max_cuts(n: int, p: Params) -> int:
+    return 0 if n == 0 else -(-n // p.min_size)
+
+
+def chunk(data, p: Params, return_examined: bool = False):
+    """Literal C oracle over one stream.  Returns uint64 exclusive cut offsets."""
+    p.check()
+    b = _as_u8(data)
+    n = int(b.size)
+    cap = max_cuts(n, p) + 1
+    cuts = np.empty(cap, dtype=np.uint64)
+    ex = ctypes.c_uint64(0)
+    k = _load().oracle_chunk(b.ctypes.data, n, p.mode, p.seq_length, p.skip_trigger,
+                             p.skip_size, p.min_size, p.max_size, cuts.ctypes.data, cap,
+                             ctypes.addressof(ex))
+    if k < 0:
+        raise RuntimeError(f"oracle_chunk failed ({k})")
+    out = cuts[:k].copy()
+    return (out, int(ex.value)) if return_examined else out
+
+
+def next_cut(data, base: int, p: Params) -> int:
+    """f(base): the single cut ending the chunk that starts at ``base``."""
+    b = _as_u8(data)
+    if not 0 <= base < b.size:
+        raise ValueError("base out of range")
+    return int(_load().oracle_next_cut(b.ctypes.data, b.size, base, p.mode, p.seq_length,
+                                       p.skip_trigger, p.skip_size, p.min_size, p.max_size,
+                                       None))
+
+
+def chunk_batch(data, offsets, p: Params):
+    """Independent streams data[offsets[j]:offsets[j+1]]; absolute cuts + cut index."""
+    p.check()
+    b = _as_u8(data)
+    off = np.ascontiguousarray(np.asarray(offsets, dtype=np.uint64))
+    ns = off.size - 1
+    cap = sum(max_cuts(int(off[j + 1] - off[j]), p) for j in range(ns)) + 1
+    cuts = np.empty(cap, dtype=np.uint64)
+    idx = np.empty(ns + 1, dtype=np.uint64)
+    k = _load().oracle_chunk_batch(b.ctypes.data, off.ctypes.data, ns, p.mode, p.seq_length,
+                                   p.skip_trigger, p.skip_size, p.min_size, p.max_size,
+                                   cuts.ctypes.data, cap, idx.ctypes.data)
+    if k < 0:
+        raise RuntimeError(f"oracle_chunk_batch failed ({k})")
+    return cuts[:k].copy(), idx
+
+
+# --------------------------------------------------------------------------
+# Pure-Python twin of the literal loop (small inputs only).
+# --------------------------------------------------------------------------
+def chunk_py(data, p: Params) -> list:
+    p.check()
+    b = bytes(_as_u8(data))
+    n = len(b)
+    L, T, S = p.seq_length, p.skip_trigger, p.skip_size
+    cuts, base = [], 0
+    while base < n:
+        limit = min(base + p.max_size, n)
+        i = base + p.min_size - L
+        run, opp = 1, 0
+        while True:
+            if i + 1 >= limit:
+                cut = limit
+                break
+            x, y = b[i], b[i + 1]
+            fav = x < y if p.mode == INCREASING else x > y
+            opn = x > y if p.mode == INCREASING else x < y
+            if fav:
+                run += 1
+                if run == L:
+                    cut = i + 2
+                    break
+                i += 1
+            elif opn:
+                run, opp = 1, opp + 1
+                if opp == T:                       # P:189, reading c2
+                    i, run, opp = i + 1 + S, 1, 0  # reading c3
+                    continue
+                i += 1
+            else:
+                run = 1
+                i += 1
+        cuts.append(cut)
+        base = cut
+    return cuts
+
+
+# --------------------------------------------------------------------------
+# Query formulation (structurally different; numpy).
+#
+# combine the L-1 "favourable" masks with AND; a set bit k means
+# bytes k..k+L-1 are strictly monotone; the boundary is L bytes past k.
+# the skip position is the n-th set bit of the opposing mask, n =
+# the SkipTrigger-th opposing pair counted from the scan anchor.
+# Per chunk: anchor a = base+min-L; among pairs a..limit-2 take the first run
+# start k >= a (cut k+L) and the T-th opposing pair d >= a; the earlier event
+# wins; a skip re-anchors at d+1+S.
+# --------------------------------------------------------------------------
+def chunk_query(data, p: Params) -> np.ndarray:
+    p.check()
+    b = _as_u8(data).astype(np.int16)
+    n = int(b.size)
+    L, T, S = p.seq_length, p.skip_trigger, p.skip_size
+    if n == 0:
+        return np.zeros(0, dtype=np.uint64)
+    diff = b[1:] - b[:-1] if n > 1 else np.zeros(0, dtype=np.int16)
+    if p.mode == INCREASING:
+        fav, opn = diff > 0, diff < 0
+    else:
+        fav, opn = diff < 0, diff > 0
+    # run_start[k] = bytes k..k+L-1 strictly monotone  <=> fav[k..k+L-2] all set
+    cs = np.concatenate([[0], np.cumsum(fav, dtype=np.int64)])
+    m = L - 1
+    npairs = fav.size
+    if npairs >= m:
+        ks = np.arange(0, npairs - m + 1)
+        run_start = np.nonzero(cs[ks + m] - cs[ks] == m)[0]
+    else:
+        run_start = np.zeros(0, dtype=np.int64)
+    opp_pos = np.nonzero(opn)[0]
+    cuts = []
+    base = 0
+    while base < n:
+        limit = min(base + p.max_size, n)
+        a = base + p.min_size - L
+        while True:
+            last_pair = limit - 2                       # pairs a..last_pair are examined
+            if a > last_pair:
+                cut = limit
+                break
+            j = np.searchsorted(run_start, a)
+            k = int(run_start[j]) if j < run_start.size else None
+            if k is not None and k + m - 1 > last_pair:  # run must end by pair last_pair
+                k = None
+            q = np.searchsorted(opp_pos, a) + T - 1
+            d = int(opp_pos[q]) if q < opp_pos.size else None
+            if d is not None and d > last_pair:
+                d = None
+            if k is not None and (d is None or k + m - 1 < d):
+                cut = k + L
+                break
+            if d is not None:
+                a = d + 1 + S
+                continue
+            cut = limit
+            break
+        cuts.append(cut)
+        base = cut
+    return np.asarray(cuts, dtype=np.uint64)
