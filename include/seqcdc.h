@@ -1,0 +1,146 @@
+/*
+ * seqcdc.h -- C ABI of the B200-native SeqCDC boundary-detection library
+ * (libseqcdc.so, built from paper_2505_21194_b200/csrc/).
+ *
+ * The operation is SeqCDC chunking (Udayashankar & Al-Kiswany, "Vectorized
+ * Sequence-Based Chunking for Data Deduplication", arXiv 2505.21194;
+ * PAPER.md lines are cited as P:n):
+ *
+ *   A stream is split into chunks; a chunk boundary is inserted right after
+ *   the first run of SeqLength bytes that is strictly increasing (Increasing
+ *   mode) or strictly decreasing (Decreasing mode) (§3.1).  Each
+ *   chunk's scan starts (min_size - SeqLength) bytes after the chunk start
+ *   (§3.2).  Whenever SkipTrigger pairs of adjacent bytes in the
+ *   opposing order have been counted since the scan (re)started, the scan
+ *   jumps SkipSize bytes ahead and resets its counters (§3.3;
+ *   P:225-231).  If no boundary is found first, the chunk ends at
+ *   chunk start + max_size (§4).  The last chunk ends at the end of the
+ *   stream.  The readings of the paper's ambiguous points (SeqLength counts
+ *   bytes; skip when the count REACHES SkipTrigger; the scan resumes SkipSize
+ *   bytes past the second byte of the triggering pair; equal bytes are neither
+ *   favourable nor opposing; unsigned byte order) are listed in DESIGN.md.
+ *
+ * Conventions for every entry point:
+ *   - Pointers named d_* are DEVICE pointers (cudaMalloc / PyTorch CUDA
+ *     memory) on the current CUDA device; h_* are host pointers.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  All device work is enqueued on it; the host never blocks.
+ *     Results are valid once the stream has been synchronised.
+ *   - Cut offsets are uint64 EXCLUSIVE chunk ends, strictly increasing; for a
+ *     non-empty stream the last cut equals its length.  An empty stream has
+ *     no cuts.  The result is a pure function of (bytes, params): it does not
+ *     depend on alignment, segmenting, batch layout or GPU count.
+ *   - Return codes: SEQCDC_OK, or an error detected on the host BEFORE any
+ *     work is enqueued (nothing is launched then).  Asynchronous CUDA faults
+ *     surface at the next synchronisation, per CUDA convention.
+ *   - No exceptions cross the ABI.  Calls are thread-safe and reentrant;
+ *     concurrent calls on different streams are allowed.
+ *   - Memory: the caller owns every pointer it passes.  If d_workspace is
+ *     NULL the library takes scratch memory from its own per-device,
+ *     stream-ordered pool (cudaMallocFromPoolAsync/cudaFreeAsync on `stream`)
+ *     and keeps no pointer after the enqueued work completes.
+ */
+#ifndef SEQCDC_H_
+#define SEQCDC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEQCDC_OK 0
+#define SEQCDC_EINVAL 1   /* bad parameters or arguments */
+#define SEQCDC_ENOMEM 2   /* workspace allocation failed or too small */
+#define SEQCDC_ECUDA 3    /* a CUDA call failed while enqueuing */
+
+#define SEQCDC_INCREASING 0
+#define SEQCDC_DECREASING 1
+#define SEQCDC_MAX_SEQ_LENGTH 16   /* implementation limit on SeqLength */
+
+/* Written to *d_ncuts if the device detects inconsistent batch offsets
+ * (non-monotone, or d_offsets[ns]-d_offsets[0] != total_bytes). */
+#define SEQCDC_NCUTS_BAD_INPUT UINT64_MAX
+
+/* SeqCDC parameters ("SeqLength, SkipTrigger and SkipSize"; Table I,
+ * P:291-306; min/max chunk sizes P:378). */
+typedef struct seqcdc_params {
+    uint32_t mode;          /* SEQCDC_INCREASING or SEQCDC_DECREASING      */
+    uint32_t seq_length;    /* L: bytes in a qualifying strict run, 2..16 */
+    uint32_t skip_trigger;  /* T: opposing pairs that trigger a skip, >= 1 */
+    uint32_t skip_size;     /* S: bytes jumped past the triggering pair's second
+                               byte; 0 disables skipping                    */
+    uint64_t min_size;      /* >= L; scanning starts at chunk start + min - L */
+    uint64_t max_size;      /* >= min_size; forced cut                        */
+    uint32_t flags;         /* reserved, must be 0                                   */
+    uint32_t reserved;      /* must be 0                                             */
+} seqcdc_params_t;
+
+/* SEQCDC_OK if *p is acceptable, SEQCDC_EINVAL otherwise (mode not 0/1,
+ * L < 2 or L > SEQCDC_MAX_SEQ_LENGTH, T == 0, min < L, max < min, flags or
+ * reserved != 0, p == NULL). */
+int seqcdc_validate_params(const seqcdc_params_t *p);
+
+/* Table I row for avg_kib in {4, 8, 16} with min = avg/2 and
+ * max = 2*avg (BASELINE.json configs; the paper's 1 KB min at 4 KB, is
+ * not used).  SEQCDC_EINVAL for other sizes or a bad mode. */
+int seqcdc_default_params(uint32_t avg_kib, uint32_t mode, seqcdc_params_t *out);
+
+/* Upper bound on the number of cuts of one n-byte stream: ceil(n / min)
+ * (every non-final chunk has >= min bytes); 0 for n == 0. */
+uint64_t seqcdc_max_cuts(uint64_t n, const seqcdc_params_t *p);
+
+/* Upper bound on the cuts of a batch: total_bytes / min + nstreams. */
+uint64_t seqcdc_max_cuts_batch(uint64_t total_bytes, uint32_t nstreams, const seqcdc_params_t *p);
+
+/* Bytes of device scratch a call with these sizes needs (pass a buffer of at
+ * least this size as d_workspace to avoid the internal pool). */
+size_t seqcdc_workspace_size(uint64_t total_bytes, uint32_t nstreams, const seqcdc_params_t *p);
+
+/*
+ * Chunk one stream d_in[0..n).
+ *   d_in     device, any alignment, n bytes, read-only.
+ *   d_cuts   device uint64[seqcdc_max_cuts(n, p)] (capacity is a documented
+ *            precondition the device cannot check).
+ *   d_ncuts  device uint64[1]: number of cuts written.
+ *   d_workspace/ws_bytes: optional caller scratch (see above), else NULL/0.
+ * Errors: SEQCDC_EINVAL (bad params, NULL pointers with n > 0),
+ * SEQCDC_ENOMEM, SEQCDC_ECUDA.
+ */
+int seqcdc_chunk(const uint8_t *d_in, uint64_t n, const seqcdc_params_t *p,
+                 uint64_t *d_cuts, uint64_t *d_ncuts,
+                 void *d_workspace, size_t ws_bytes, void *stream);
+
+/*
+ * Chunk `nstreams` independent streams ("files are chunked independently";
+ * boundaries never span streams).  Stream j is d_in[d_offsets[j] ..
+ * d_offsets[j+1]); d_offsets is a device uint64[nstreams+1], non-decreasing,
+ * and total_bytes must equal d_offsets[nstreams] - d_offsets[0] (the host
+ * sizes the work from it).  Cuts are written stream after stream as offsets
+ * into d_in (i.e. absolute: d_offsets[j] + local cut); stream j's cuts are
+ * d_cuts[d_cut_index[j] .. d_cut_index[j+1]) with d_cut_index a device
+ * uint64[nstreams+1]; *d_ncuts = total.  d_cuts capacity:
+ * seqcdc_max_cuts_batch(total_bytes, nstreams, p).
+ */
+int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t nstreams,
+                       uint64_t total_bytes, const seqcdc_params_t *p,
+                       uint64_t *d_cuts, uint64_t *d_cut_index, uint64_t *d_ncuts,
+                       void *d_workspace, size_t ws_bytes, void *stream);
+
+/* Testing / tuning knob: force the segment length G (rounded up to a
+ * multiple of max_size, and to at least max_size) used to split streams into
+ * speculative chains; 0 restores the automatic choice.  Process-global.  The
+ * cut list never depends on it (tests/test_gpu_parity.py checks this). */
+int seqcdc_set_segment_bytes(uint64_t g);
+
+/* Human-readable name of a return code (static string). */
+const char *seqcdc_strerror(int code);
+
+/* Library build/tuning info (static string: tile/stage sizes, arch). */
+const char *seqcdc_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SEQCDC_H_ */

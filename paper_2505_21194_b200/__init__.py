@@ -1,0 +1,220 @@
+"""B200-native SeqCDC boundary detection (arXiv 2505.21194) -- Python binding.
+
+Thin ctypes binding over the C ABI in ``include/seqcdc.h`` (libseqcdc.so,
+built in-tree from ``csrc/``).  Argument marshalling only: every step of the
+chunking path runs in the library's CUDA kernels.  PyTorch supplies device
+memory and streams.  There is no CPU fallback: if the extension is missing or
+no CUDA device is present, calls raise.
+
+Names follow the paper: ``mode`` (Increasing/Decreasing),
+``seq_length`` (SeqLength), ``skip_trigger`` (SkipTrigger), ``skip_size``
+(SkipSize), ``min_size``/``max_size``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+from . import _build
+
+INCREASING = 0
+DECREASING = 1
+
+SEQCDC_OK, SEQCDC_EINVAL, SEQCDC_ENOMEM, SEQCDC_ECUDA = 0, 1, 2, 3
+NCUTS_BAD_INPUT = (1 << 64) - 1
+
+# Every symbol include/seqcdc.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "seqcdc_validate_params", "seqcdc_default_params", "seqcdc_max_cuts", "seqcdc_max_cuts_batch",
+    "seqcdc_workspace_size", "seqcdc_chunk", "seqcdc_chunk_batch", "seqcdc_strerror",
+    "seqcdc_build_info", "seqcdc_set_segment_bytes",
+)
+
+
+class _CParams(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_uint32), ("seq_length", ctypes.c_uint32),
+                ("skip_trigger", ctypes.c_uint32), ("skip_size", ctypes.c_uint32),
+                ("min_size", ctypes.c_uint64), ("max_size", ctypes.c_uint64),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+@dataclass(frozen=True)
+class SeqParams:
+    """SeqCDC parameters (Table I)."""
+
+    mode: int = INCREASING
+    seq_length: int = 5
+    skip_trigger: int = 50
+    skip_size: int = 256
+    min_size: int = 4096
+    max_size: int = 16384
+
+    def c(self) -> _CParams:
+        return _CParams(self.mode, self.seq_length, self.skip_trigger, self.skip_size,
+                        self.min_size, self.max_size, 0, 0)
+
+    @staticmethod
+    def table1(avg_kib: int, mode: int = INCREASING) -> "SeqParams":
+        cp = _CParams()
+        _check(lib().seqcdc_default_params(avg_kib, mode, ctypes.byref(cp)), "seqcdc_default_params")
+        return SeqParams(cp.mode, cp.seq_length, cp.skip_trigger, cp.skip_size, cp.min_size, cp.max_size)
+
+
+class SeqCDCError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load libseqcdc.so (building it in-tree first if sources are newer)."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if _build.stale():
+            path = _build.build()
+        if not os.path.exists(path):
+            raise SeqCDCError(f"libseqcdc.so missing at {path}; run __graft_entry__.build()")
+        L = ctypes.CDLL(path)
+        u32, u64, p, sz = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t
+        P = ctypes.POINTER(_CParams)
+        L.seqcdc_validate_params.argtypes = [P]
+        L.seqcdc_validate_params.restype = ctypes.c_int
+        L.seqcdc_default_params.argtypes = [u32, u32, P]
+        L.seqcdc_default_params.restype = ctypes.c_int
+        L.seqcdc_max_cuts.argtypes = [u64, P]
+        L.seqcdc_max_cuts.restype = u64
+        L.seqcdc_max_cuts_batch.argtypes = [u64, u32, P]
+        L.seqcdc_max_cuts_batch.restype = u64
+        L.seqcdc_workspace_size.argtypes = [u64, u32, P]
+        L.seqcdc_workspace_size.restype = sz
+        L.seqcdc_chunk.argtypes = [p, u64, P, p, p, p, sz, p]
+        L.seqcdc_chunk.restype = ctypes.c_int
+        L.seqcdc_chunk_batch.argtypes = [p, p, u32, u64, P, p, p, p, p, sz, p]
+        L.seqcdc_chunk_batch.restype = ctypes.c_int
+        L.seqcdc_strerror.argtypes = [ctypes.c_int]
+        L.seqcdc_strerror.restype = ctypes.c_char_p
+        L.seqcdc_build_info.argtypes = []
+        L.seqcdc_build_info.restype = ctypes.c_char_p
+        L.seqcdc_set_segment_bytes.argtypes = [u64]
+        L.seqcdc_set_segment_bytes.restype = ctypes.c_int
+        if hasattr(L, "seqcdc_range_chunk"):
+            L.seqcdc_range_chunk.argtypes = [p, u64, u64, u64, u64, u32, P, p, p, p, sz, p]
+            L.seqcdc_range_chunk.restype = ctypes.c_int
+            L.seqcdc_range_max_cuts.argtypes = [u64, u64, P]
+            L.seqcdc_range_max_cuts.restype = u64
+            L.seqcdc_range_finalize.argtypes = [p, p, p, p, u32, p]
+            L.seqcdc_range_finalize.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != SEQCDC_OK:
+        raise SeqCDCError(f"{what}: {lib().seqcdc_strerror(rc).decode()} ({rc})")
+
+
+def validate(p: SeqParams) -> bool:
+    cp = p.c()
+    return lib().seqcdc_validate_params(ctypes.byref(cp)) == SEQCDC_OK
+
+
+def max_cuts(n: int, p: SeqParams) -> int:
+    cp = p.c()
+    return int(lib().seqcdc_max_cuts(n, ctypes.byref(cp)))
+
+
+def max_cuts_batch(total: int, nstreams: int, p: SeqParams) -> int:
+    cp = p.c()
+    return int(lib().seqcdc_max_cuts_batch(total, nstreams, ctypes.byref(cp)))
+
+
+def workspace_size(total: int, nstreams: int, p: SeqParams) -> int:
+    cp = p.c()
+    return int(lib().seqcdc_workspace_size(total, nstreams, ctypes.byref(cp)))
+
+
+def set_segment_bytes(g: int) -> None:
+    """Force the speculative segment length (testing/tuning); 0 = automatic."""
+    _check(lib().seqcdc_set_segment_bytes(int(g)), "seqcdc_set_segment_bytes")
+
+
+def build_info() -> str:
+    return lib().seqcdc_build_info().decode()
+
+
+def _stream_ptr(stream, device):
+    import torch
+    s = torch.cuda.current_stream(device) if stream is None else stream
+    return s.cuda_stream
+
+
+def _require_cuda(t, name):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise SeqCDCError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if not t.is_contiguous():
+        raise SeqCDCError(f"{name} must be contiguous")
+
+
+def chunk_into(data, p: SeqParams, cuts, ncuts, workspace=None, stream=None) -> None:
+    """Asynchronous: enqueue seqcdc_chunk on ``stream``.  ``data`` uint8 CUDA,
+    ``cuts`` int64 CUDA with >= max_cuts(n) entries, ``ncuts`` int64 CUDA [1]."""
+    import torch
+    _require_cuda(data, "data")
+    if data.dtype != torch.uint8:
+        raise SeqCDCError("data must be uint8")
+    n = data.numel()
+    cp = p.c()
+    ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    rc = lib().seqcdc_chunk(data.data_ptr() if n else None, n, ctypes.byref(cp),
+                            cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(), ws_ptr, ws_len,
+                            _stream_ptr(stream, data.device))
+    _check(rc, "seqcdc_chunk")
+
+
+def chunk(data, p: SeqParams, stream=None):
+    """Cut offsets (int64 CUDA tensor) of one stream.  Synchronises to size the result."""
+    import torch
+    _require_cuda(data, "data")
+    n = data.numel()
+    cuts = torch.empty(max(max_cuts(n, p), 1), dtype=torch.int64, device=data.device)
+    ncuts = torch.zeros(1, dtype=torch.int64, device=data.device)
+    chunk_into(data, p, cuts, ncuts, stream=stream)
+    k = int(ncuts.item())
+    return cuts[:k]
+
+
+def chunk_batch_into(data, offsets, p: SeqParams, cuts, cut_index, ncuts, total=None, workspace=None,
+                     stream=None) -> None:
+    """Asynchronous batch call.  ``offsets`` int64 CUDA [ns+1]; cuts are absolute offsets into data."""
+    import torch
+    _require_cuda(data, "data")
+    _require_cuda(offsets, "offsets")
+    ns = offsets.numel() - 1
+    if total is None:
+        total = int(offsets[-1].item() - offsets[0].item())
+    cp = p.c()
+    ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    rc = lib().seqcdc_chunk_batch(data.data_ptr() if data.numel() else None, offsets.data_ptr(), ns, total,
+                                  ctypes.byref(cp), cuts.data_ptr() if cuts.numel() else None,
+                                  cut_index.data_ptr(), ncuts.data_ptr(), ws_ptr, ws_len,
+                                  _stream_ptr(stream, data.device))
+    _check(rc, "seqcdc_chunk_batch")
+
+
+def chunk_batch(data, offsets, p: SeqParams, stream=None):
+    """Independent streams data[offsets[j]:offsets[j+1]] -> (cuts, cut_index), int64 CUDA tensors."""
+    import torch
+    ns = offsets.numel() - 1
+    total = int(offsets[-1].item() - offsets[0].item())
+    cuts = torch.empty(max(max_cuts_batch(total, ns, p), 1), dtype=torch.int64, device=data.device)
+    cut_index = torch.empty(ns + 1, dtype=torch.int64, device=data.device)
+    ncuts = torch.zeros(1, dtype=torch.int64, device=data.device)
+    chunk_batch_into(data, offsets, p, cuts, cut_index, ncuts, total=total, stream=stream)
+    k = int(ncuts.item())
+    if k == NCUTS_BAD_INPUT - (1 << 64):
+        raise SeqCDCError("inconsistent batch offsets")
+    return cuts[:k], cut_index
