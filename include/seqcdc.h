@@ -134,6 +134,15 @@ int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t 
  * cut list never depends on it (tests/test_gpu_parity.py checks this). */
 int seqcdc_set_segment_bytes(uint64_t g);
 
+/* Profiling (used by bench.py): when enabled, each call records CUDA events
+ * on its stream around its phases.  seqcdc_profile_collect() synchronises on
+ * them and writes summed milliseconds ms[0] = segment setup, ms[1] = the walk
+ * kernel (the hot loop), ms[2] = stitch + fallback + scan + copy, ms[3] = whole
+ * call, and the number of calls; it then clears the records.  Enabling or
+ * disabling also clears them.  Process-global. */
+int seqcdc_profile_enable(int on);
+int seqcdc_profile_collect(double *ms, uint64_t *ncalls);
+
 /* Human-readable name of a return code (static string). */
 const char *seqcdc_strerror(int code);
 

@@ -28,7 +28,7 @@ NCUTS_BAD_INPUT = (1 << 64) - 1
 EXPORTS = (
     "seqcdc_validate_params", "seqcdc_default_params", "seqcdc_max_cuts", "seqcdc_max_cuts_batch",
     "seqcdc_workspace_size", "seqcdc_chunk", "seqcdc_chunk_batch", "seqcdc_strerror",
-    "seqcdc_build_info", "seqcdc_set_segment_bytes",
+    "seqcdc_build_info", "seqcdc_set_segment_bytes", "seqcdc_profile_enable", "seqcdc_profile_collect",
 )
 
 
@@ -100,6 +100,10 @@ def lib():
         L.seqcdc_build_info.restype = ctypes.c_char_p
         L.seqcdc_set_segment_bytes.argtypes = [u64]
         L.seqcdc_set_segment_bytes.restype = ctypes.c_int
+        L.seqcdc_profile_enable.argtypes = [ctypes.c_int]
+        L.seqcdc_profile_enable.restype = ctypes.c_int
+        L.seqcdc_profile_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
+        L.seqcdc_profile_collect.restype = ctypes.c_int
         if hasattr(L, "seqcdc_range_chunk"):
             L.seqcdc_range_chunk.argtypes = [p, u64, u64, u64, u64, u32, P, p, p, p, sz, p]
             L.seqcdc_range_chunk.restype = ctypes.c_int
@@ -139,6 +143,18 @@ def workspace_size(total: int, nstreams: int, p: SeqParams) -> int:
 def set_segment_bytes(g: int) -> None:
     """Force the speculative segment length (testing/tuning); 0 = automatic."""
     _check(lib().seqcdc_set_segment_bytes(int(g)), "seqcdc_set_segment_bytes")
+
+
+def profile_enable(on: bool = True) -> None:
+    _check(lib().seqcdc_profile_enable(1 if on else 0), "seqcdc_profile_enable")
+
+
+def profile_collect():
+    """-> (dict of summed ms per phase, number of calls) since profile_enable()."""
+    ms = (ctypes.c_double * 4)()
+    n = ctypes.c_uint64(0)
+    _check(lib().seqcdc_profile_collect(ms, ctypes.byref(n)), "seqcdc_profile_collect")
+    return {"setup": ms[0], "walk": ms[1], "post": ms[2], "call": ms[3]}, int(n.value)
 
 
 def build_info() -> str:

@@ -1,24 +1,27 @@
 // seqcdc.cu -- B200 (sm_100a) SeqCDC chunking behind the C ABI in include/seqcdc.h.
 //
 // Pipeline for one call (all on the caller's stream, no host synchronisation):
-//   1. k_setup     segment table: each stream is cut into segments of G bytes
-//                  (G a multiple of max_size); list capacities; state reset.
-//   2. k_walk      persistent CTAs, one warp each.  Each CTA takes segments in
-//                  order and walks a SPECULATIVE chain from the segment start as
-//                  if a cut were there ("the next cut depends only on the
+//   0. reset       one cudaMemsetAsync of the control words + publication
+//                  counters (single stream), or k_setup (batch): the segment
+//                  table -- each stream cut into segments of G bytes, G a
+//                  multiple of max_size.
+//   1. k_walk      persistent CTAs, one warp each.  A CTA takes segments in
+//                  order and walks a SPECULATIVE chain from the segment start
+//                  as if a cut were there ("the next cut depends only on the
 //                  previous cut"), recording cuts < segment end in its list L_s
 //                  (published every 32 cuts with release semantics).  At the
 //                  first cut >= segment end the chain continues (EXTENSION),
-//                  each cut checked against the list of the chain that owns that
-//                  region; the first common cut is a merge point: from there on
-//                  both chains are identical.  Extension cuts go to X_s.
-//   3. k_stitch    per stream: follow the merges from the stream start (the
-//                  only chain that is right from its start) to mark live
-//                  chains and where each becomes valid; count valid cuts.
-//   4. k_fallback  streams whose extension overflowed its budget (pathological
-//                  phase-locked data) are re-walked by one warp end to end.
-//   5. k_scan      exclusive scan of per-segment counts -> output offsets.
-//   6. k_copy      gather valid L/X cuts into d_cuts.
+//                  each cut checked against the list of the chain that owns
+//                  that region; the first common cut is a merge point: from
+//                  there on both chains are identical.  Extension cuts go to X_s.
+//   2. k_stitch    per stream (one CTA): follow the merges from the stream start
+//                  (the only chain that is right from its start) to mark live
+//                  chains and where each becomes valid; count valid cuts.  A
+//                  stream whose extension overflowed its budget (pathological
+//                  phase-locked data) is re-walked here by one warp, end to end.
+//                  For a single stream the same CTA also scans the counts.
+//   3. k_scan      (batches only) exclusive scan of per-segment counts.
+//   4. k_copy      gather valid L/X cuts into d_cuts.
 // The hot loop (k_walk) streams every byte HBM->SMEM once with 1-D TMA and
 // classifies lazily; see seqcdc_device.cuh.
 #include <cuda_runtime.h>
@@ -26,8 +29,10 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/seqcdc.h"
 #include "seqcdc_device.cuh"
@@ -38,32 +43,36 @@ namespace seqcdc {
 
 constexpr uint64_t DONE_BIT = 1ull << 63;
 constexpr uint64_t CNT_MASK = DONE_BIT - 1;
-constexpr int32_t TGT_UNSET = -1;
 constexpr int32_t TGT_END = -2;
 constexpr int32_t TGT_OVERFLOW = -3;
 constexpr int64_t ENTRY_DEAD = -2;
-constexpr uint32_t K_EXT = 4;            // extension budget, in segments
-constexpr uint64_t G_FLOOR_CHUNKS = 32;  // minimum segment length, in max_size units
+constexpr uint32_t K_EXT = 4;             // extension budget, in segments
+constexpr uint64_t G_FLOOR_CHUNKS = 32;   // minimum segment length, in max_size units
+constexpr uint64_t G_CEIL = 256ull << 20; // keeps a chain's span far below REBASE_AT
+constexpr uint32_t STITCH_MAX_SEGS = 8000;
 
-enum { C_NSEG = 0, C_NEXT = 1, C_NEXT_FB = 2, C_NFLAG = 3, C_BAD = 4, C_NWORDS = 8 };
+enum { C_NSEG = 0, C_NEXT = 1, C_NFLAG = 2, C_BAD = 3, C_NWORDS = 8 };
 
 struct Work {
     // inputs
     const uint8_t *in;
     const uint64_t *offs;  // [ns+1]
     uint32_t ns;
+    uint32_t single;       // 1: one stream at offset 0, segment table is arithmetic
+    uint32_t nseg1;        // single: number of segments
+    uint32_t capL1, capX1; // single: uniform list capacities
     uint64_t G;
     uint64_t total;
     DevParams p;
-    // per stream
+    // per stream (batch)
     uint32_t *str_first;   // [ns+1]
     uint32_t *str_flag;    // [ns]
-    uint32_t *flagged;     // [ns]
-    // per segment
+    // per segment (batch)
     uint64_t *seg_lo, *seg_hi;
     uint32_t *seg_stream;
     uint64_t *Loff, *Xoff;
     uint32_t *Lcap, *Xcap;
+    // per segment (both)
     uint64_t *Lcnt;        // published: count | DONE_BIT
     uint32_t *Xcnt;
     int32_t *target;
@@ -77,8 +86,56 @@ struct Work {
     uint64_t *cuts, *cut_index, *ncuts;
 };
 
+struct Seg {
+    uint64_t lo, hi, S0, E;   // segment [lo,hi), stream [S0,E) -- offsets into `in`
+    uint64_t Loff, Xoff;
+    uint32_t Lcap, Xcap;
+    uint32_t j, first, nseg;  // stream, its first segment, its segment count
+    bool last;
+};
+
+__device__ __forceinline__ uint32_t nseg_total(const Work &w) { return w.single ? w.nseg1 : w.ctrl[C_NSEG]; }
+
+__device__ __forceinline__ Seg get_seg(const Work &w, uint32_t s)
+{
+    Seg g;
+    if (w.single) {
+        g.j = 0;
+        g.first = 0;
+        g.nseg = w.nseg1;
+        g.S0 = 0;
+        g.E = w.total;
+        g.last = (s + 1 == w.nseg1);
+        g.lo = (uint64_t)s * w.G;
+        g.hi = g.last ? g.E : g.lo + w.G;
+        g.Lcap = w.capL1;
+        g.Loff = (uint64_t)s * w.capL1;
+        g.Xcap = g.last ? 0 : w.capX1;
+        g.Xoff = (uint64_t)s * w.capX1;
+    } else {
+        g.j = w.seg_stream[s];
+        g.first = w.str_first[g.j];
+        g.nseg = w.str_first[g.j + 1] - g.first;
+        g.last = (s + 1 == g.first + g.nseg);
+        g.S0 = w.offs[g.j];
+        g.E = w.offs[g.j + 1];
+        g.lo = w.seg_lo[s];
+        g.hi = w.seg_hi[s];
+        g.Lcap = w.Lcap[s];
+        g.Loff = w.Loff[s];
+        g.Xcap = w.Xcap[s];
+        g.Xoff = w.Xoff[s];
+    }
+    return g;
+}
+
+__device__ __forceinline__ uint64_t seg_start(const Work &w, const Seg &g, uint32_t t)
+{
+    return g.S0 + (uint64_t)(t - g.first) * w.G;
+}
+
 // ------------------------------------------------------------------ block scan helper
-// Exclusive scan over n items with a 1024-thread block; get(i) -> u64, put(i, excl).
+// Exclusive scan over n items with the whole block; get(i) -> u64, put(i, excl).
 template <typename Get, typename Put>
 __device__ uint64_t block_scan(uint64_t n, Get get, Put put)
 {
@@ -98,13 +155,13 @@ __device__ uint64_t block_scan(uint64_t n, Get get, Put put)
         if (lane == 31) warp_tot[wid] = incl;
         __syncthreads();
         if (wid == 0) {
-            uint64_t w = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0, wi = w;
+            uint64_t x = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0, xi = x;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                uint64_t t = __shfl_up_sync(FULL, wi, o);
-                if (lane >= o) wi += t;
+                uint64_t t = __shfl_up_sync(FULL, xi, o);
+                if (lane >= o) xi += t;
             }
-            warp_tot[lane] = wi - w;
+            warp_tot[lane] = xi - x;
         }
         __syncthreads();
         const uint64_t base = carry;
@@ -116,7 +173,7 @@ __device__ uint64_t block_scan(uint64_t n, Get get, Put put)
     return carry;
 }
 
-// ------------------------------------------------------------------ 1. setup
+// ------------------------------------------------------------------ 0. setup (batches)
 __global__ void __launch_bounds__(1024) k_setup(Work w)
 {
     const uint64_t G = w.G, mn = w.p.mn;
@@ -133,7 +190,6 @@ __global__ void __launch_bounds__(1024) k_setup(Work w)
         }
         return;
     }
-    // segments per stream -> first segment index
     uint64_t nseg = block_scan(
         w.ns,
         [&](uint64_t j) -> uint64_t {
@@ -145,12 +201,10 @@ __global__ void __launch_bounds__(1024) k_setup(Work w)
         w.str_first[w.ns] = (uint32_t)nseg;
         w.ctrl[C_NSEG] = (uint32_t)nseg;
         w.ctrl[C_NEXT] = 0;
-        w.ctrl[C_NEXT_FB] = 0;
         w.ctrl[C_NFLAG] = 0;
         w.ctrl[C_BAD] = 0;
     }
     __syncthreads();
-    // per segment: bounds, capacities, state
     for (uint64_t s = threadIdx.x; s < nseg; s += blockDim.x) {
         uint32_t lo = 0, hi = w.ns;  // largest j with str_first[j] <= s
         while (hi - lo > 1) {
@@ -161,19 +215,16 @@ __global__ void __launch_bounds__(1024) k_setup(Work w)
         const uint64_t k = s - w.str_first[j];
         const uint64_t S0 = w.offs[j], E = w.offs[j + 1];
         const uint64_t a = S0 + k * G;
-        const uint64_t b = (a + G < E) ? a + G : E;
         const bool last = (s + 1 == w.str_first[j + 1]);
+        const uint64_t b = last ? E : a + G;
         w.seg_lo[s] = a;
-        w.seg_hi[s] = last ? E : b;
+        w.seg_hi[s] = b;
         w.seg_stream[s] = j;
-        w.Lcap[s] = (uint32_t)(((last ? E : b) - a) / mn + 2);
+        w.Lcap[s] = (uint32_t)((b - a) / mn + 2);
         uint64_t xr = last ? 0 : E - b;
         if (xr > K_EXT * G) xr = K_EXT * G;
         w.Xcap[s] = last ? 0 : (uint32_t)(xr / mn + 2);
         w.Lcnt[s] = 0;
-        w.Xcnt[s] = 0;
-        w.target[s] = TGT_UNSET;
-        w.midx[s] = -1;
     }
     __syncthreads();
     block_scan(nseg, [&](uint64_t s) -> uint64_t { return w.Lcap[s]; },
@@ -182,7 +233,7 @@ __global__ void __launch_bounds__(1024) k_setup(Work w)
                [&](uint64_t s, uint64_t ex) { w.Xoff[s] = ex; });
 }
 
-// ------------------------------------------------------------------ 2. walk
+// ------------------------------------------------------------------ 1. walk
 struct ListBuf {  // 32 cuts buffered in lane registers, written coalesced
     uint64_t v;
     uint32_t n;   // total cuts appended
@@ -201,7 +252,7 @@ __device__ __forceinline__ void lb_flush(ListBuf &b, uint64_t *dst, int lane)
     if (lane < (int)r) dst[b.n - r + lane] = b.v;
 }
 
-// Publish the first b.n entries of a spec list (release), optionally final.
+// Publish the first n entries of a spec list (release), optionally final.
 __device__ __forceinline__ void publish(uint64_t *cntp, uint32_t n, bool done, int lane)
 {
     __threadfence();
@@ -215,32 +266,33 @@ struct Cursor {
     int64_t t;     // segment whose list the window belongs to
     uint64_t j;    // list index of window entry 0
     uint32_t nv;   // valid entries in the window
-    uint64_t w;    // this lane's window entry
+    uint64_t v;    // this lane's window entry
 };
 
-// Is relative offset `rel` a cut of chain t (implicit start or in L_t)?
-__device__ int check_cut(const Work &w, Cursor &c, uint32_t t, uint64_t rel, int64_t &idx, int lane)
+// Is offset `cut` a cut of chain t (its implicit start, or an entry of L_t)?
+__device__ int check_cut(const Work &w, Cursor &c, uint32_t t, uint64_t t_lo, uint64_t Loff_t, uint64_t cut,
+                         int64_t &idx, int lane)
 {
     if ((int64_t)t != c.t) {
         c.t = t;
         c.j = 0;
         c.nv = 0;
     }
-    if (rel == w.seg_lo[t]) {
+    if (cut == t_lo) {
         idx = -1;
         return CK_MERGE;
     }
-    const uint64_t *Lt = w.L + w.Loff[t];
+    const uint64_t *Lt = w.L + Loff_t;
 #pragma unroll 1
     for (;;) {
         if (c.nv > 0) {
-            const uint32_t hit = __ballot_sync(FULL, lane < (int)c.nv && c.w == rel);
+            const uint32_t hit = __ballot_sync(FULL, lane < (int)c.nv && c.v == cut);
             if (hit) {
                 idx = (int64_t)(c.j + __ffs(hit) - 1);
                 return CK_MERGE;
             }
-            const uint64_t last = __shfl_sync(FULL, c.w, c.nv - 1);
-            if (last > rel) return CK_NO;
+            const uint64_t last = __shfl_sync(FULL, c.v, c.nv - 1);
+            if (last > cut) return CK_NO;
             if (c.nv == 32) {
                 c.j += 32;
                 c.nv = 0;
@@ -249,7 +301,7 @@ __device__ int check_cut(const Work &w, Cursor &c, uint32_t t, uint64_t rel, int
                 const uint64_t cnt = word & CNT_MASK;
                 if (cnt > c.j + c.nv) {
                     c.nv = (uint32_t)(cnt - c.j < 32 ? cnt - c.j : 32);
-                    c.w = lane < (int)c.nv ? __ldcg(Lt + c.j + lane) : 0;
+                    c.v = lane < (int)c.nv ? __ldcg(Lt + c.j + lane) : 0;
                     continue;
                 }
                 return (word & DONE_BIT) ? CK_NO : CK_UNDECIDED;
@@ -259,73 +311,93 @@ __device__ int check_cut(const Work &w, Cursor &c, uint32_t t, uint64_t rel, int
         const uint64_t cnt = word & CNT_MASK;
         if (cnt > c.j) {
             c.nv = (uint32_t)(cnt - c.j < 32 ? cnt - c.j : 32);
-            c.w = lane < (int)c.nv ? __ldcg(Lt + c.j + lane) : 0;
+            c.v = lane < (int)c.nv ? __ldcg(Lt + c.j + lane) : 0;
             continue;
         }
         return (word & DONE_BIT) ? CK_NO : CK_UNDECIDED;
     }
 }
 
-template <int MODE, bool SMALL_M>
-__device__ void walk_segment(const Work &w, Ring &rg, uint32_t s, int lane)
+__device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, int lane)
+{
+    wk.buf = smem_u32(smem);
+    wk.bar = smem_u32(smem + RING);
+    wk.pending = 0;
+    wk.nextpar = 0;
+    wk.rb = 0;
+    wk.lo_rel = wk.end_rel = 0;
+    wk.t_first = wk.t_next = wk.t_end = 0;
+    wk.res_lo = wk.res_hi = 0;
+    if (lane < STAGES) mbar_init(wk.bar + 8 * lane, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+}
+
+template <int MODE, bool LONG>
+__device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
 {
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
-    const uint32_t j = w.seg_stream[s];
-    const uint64_t S0 = w.offs[j], E = w.offs[j + 1];
-    const uint32_t first = w.str_first[j];
-    const bool last = (s + 1 == w.str_first[j + 1]);
-    const uint64_t lo = w.seg_lo[s], hi = w.seg_hi[s];
-    const uint64_t Eabs = abase + E;
-    ring_start(rg, abase + lo, Eabs, abase + lo);
-
-    uint64_t *Ls = w.L + w.Loff[s];
+    const Seg g = get_seg(w, s);
+    const uint64_t Eabs = abase + g.E;
+    uint32_t base = walker_start(wk, abase + g.lo, Eabs);
+    uint64_t *Ls = w.L + g.Loff;
     ListBuf lb{0, 0};
-    uint64_t base = abase + lo;
-    uint64_t cut = 0;
+    uint64_t cut = 0;      // offset into `in` of the latest cut
     bool extend = false;
+    // spec phase: cuts < hi belong to L_s
+    const uint64_t hi_abs = abase + g.hi;
 #pragma unroll 1
-    while (base < Eabs) {
-        cut = resolve_chunk<MODE, SMALL_M>(rg, w.p, base, Eabs, lane);
-        if (!last && cut >= abase + hi) {
+    while (wk.rb + base < Eabs) {
+        base = walker_rebase(wk, base, Eabs);
+        const uint32_t c = resolve<MODE, LONG>(wk, w.p, base, lane);
+        const uint64_t cabs = wk.rb + c;
+        cut = cabs - abase;
+        if (!g.last && cabs >= hi_abs) {
             extend = true;
+            base = c;
             break;
         }
-        lb_push(lb, cut - abase, Ls, lane);
+        lb_push(lb, cut, Ls, lane);
         if ((lb.n & 31) == 0) publish(w.Lcnt + s, lb.n, false, lane);
-        base = cut;
+        base = c;
     }
     lb_flush(lb, Ls, lane);
     publish(w.Lcnt + s, lb.n, true, lane);
     if (!extend) return;
 
     // ---- extension: walk on until a cut coincides with the chain owning it
-    uint64_t *Xs = w.X + w.Xoff[s];
-    const uint32_t xcap = w.Xcap[s];
+    uint64_t *Xs = w.X + g.Xoff;
     ListBuf xb{0, 0};
     Cursor cur{-1, 0, 0, 0};
     int32_t tgt = TGT_OVERFLOW;
     int64_t mi = -1;
+    uint64_t t_lo = 0, t_Loff = 0;
 #pragma unroll 1
     for (;;) {
-        if (xb.n == xcap) {
+        if (xb.n == g.Xcap) {
             tgt = TGT_OVERFLOW;
             break;
         }
-        const uint64_t rel = cut - abase;
-        lb_push(xb, rel, Xs, lane);
-        if (rel == E) {
+        lb_push(xb, cut, Xs, lane);
+        if (cut == g.E) {
             tgt = TGT_END;
             break;
         }
-        const uint32_t t = first + (uint32_t)((rel - S0) / w.G);
+        const uint32_t t = g.first + (uint32_t)((cut - g.S0) / w.G);
+        if ((int64_t)t != cur.t) {
+            t_lo = seg_start(w, g, t);
+            t_Loff = w.single ? (uint64_t)t * w.capL1 : w.Loff[t];
+        }
         int64_t idx;
-        if (check_cut(w, cur, t, rel, idx, lane) == CK_MERGE) {
+        if (check_cut(w, cur, t, t_lo, t_Loff, cut, idx, lane) == CK_MERGE) {
             tgt = (int32_t)t;
             mi = idx;
             break;
         }
-        base = cut;
-        cut = resolve_chunk<MODE, SMALL_M>(rg, w.p, base, Eabs, lane);
+        base = walker_rebase(wk, base, Eabs);
+        const uint32_t c = resolve<MODE, LONG>(wk, w.p, base, lane);
+        cut = wk.rb + c - abase;
+        base = c;
     }
     lb_flush(xb, Xs, lane);
     if (lane == 0) {
@@ -335,61 +407,79 @@ __device__ void walk_segment(const Work &w, Ring &rg, uint32_t s, int lane)
     }
 }
 
-template <int MODE, bool SMALL_M>
+template <int MODE, bool LONG>
 __global__ void __launch_bounds__(32) k_walk(Work w)
 {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x;
-    Ring rg;
-    rg.buf = smem_u32(smem);
-    rg.bar = smem_u32(smem + RING);
-    rg.pending = 0;
-    rg.nextpar = 0;
-    rg.t_first = rg.t_next = rg.t_end = 0;
-    rg.a_lo = rg.a_hi = 0;
-    if (lane < STAGES) mbar_init(rg.bar + 8 * lane, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
+    Walker wk;
+    walker_init(wk, smem, lane);
     if (w.ctrl[C_BAD]) return;
-    const uint32_t nseg = w.ctrl[C_NSEG];
+    const uint32_t nseg = nseg_total(w);
 #pragma unroll 1
     for (;;) {
         uint32_t s = 0;
         if (lane == 0) s = atomicAdd(w.ctrl + C_NEXT, 1u);
         s = __shfl_sync(FULL, s, 0);
         if (s >= nseg) break;
-        walk_segment<MODE, SMALL_M>(w, rg, s, lane);
+        walk_segment<MODE, LONG>(w, wk, s, lane);
     }
-    ring_drain(rg);
+    ring_drain(wk);
 }
 
-// ------------------------------------------------------------------ 3. stitch
+// ------------------------------------------------------------------ 2. stitch (+fallback, +scan for one stream)
+// One warp re-walks a whole stream (used only when an extension overflowed).
+template <int MODE, bool LONG>
+__device__ uint32_t fallback_stream(const Work &w, Walker &wk, uint64_t S0, uint64_t E, uint64_t *dst, int lane)
+{
+    const uint64_t abase = (uint64_t)(uintptr_t)w.in;
+    const uint64_t Eabs = abase + E;
+    uint32_t base = walker_start(wk, abase + S0, Eabs);
+    ListBuf lb{0, 0};
+#pragma unroll 1
+    while (wk.rb + base < Eabs) {
+        base = walker_rebase(wk, base, Eabs);
+        const uint32_t c = resolve<MODE, LONG>(wk, w.p, base, lane);
+        lb_push(lb, wk.rb + c - abase, dst, lane);
+        base = c;
+    }
+    lb_flush(lb, dst, lane);
+    ring_drain(wk);
+    return lb.n;
+}
+
+template <int MODE, bool LONG>
 __global__ void __launch_bounds__(1024) k_stitch(Work w)
 {
-    extern __shared__ __align__(16) uint8_t sm[];
-    if (w.ctrl[C_BAD]) return;
+    extern __shared__ __align__(128) uint8_t sm[];
     __shared__ uint32_t flag;
+    if (w.ctrl[C_BAD]) return;
+    // layout: [ring | barriers | tg[K] | mi[K] | en[K]]
+    int32_t *tg = (int32_t *)(sm + SMEM_WALK);
+    const uint32_t kmax = STITCH_MAX_SEGS;
+    int64_t *mi = (int64_t *)(sm + SMEM_WALK + 4 * kmax);
+    int64_t *en = (int64_t *)(sm + SMEM_WALK + 12 * kmax);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (uint32_t j = blockIdx.x; j < w.ns; j += gridDim.x) {
-        const uint32_t f = w.str_first[j], k = w.str_first[j + 1] - f;
+        const uint32_t f = w.single ? 0 : w.str_first[j];
+        const uint32_t k = w.single ? w.nseg1 : w.str_first[j + 1] - f;
         if (k == 1) {
             if (threadIdx.x == 0) {
                 w.entry[f] = -1;
                 w.seg_count[f] = w.Lcnt[f] & CNT_MASK;
-                w.str_flag[j] = 0;
+                if (!w.single) w.str_flag[j] = 0;
             }
             continue;
         }
-        int32_t *tg = (int32_t *)sm;                              // [k]
-        int64_t *en = (int64_t *)(sm + ((4ull * k + 15) & ~15ull));  // [k]
         for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
-            int32_t t = w.target[f + i];
+            const int32_t t = w.target[f + i];
             tg[i] = t >= 0 ? t - (int32_t)f : t;
+            mi[i] = w.midx[f + i];
             en[i] = ENTRY_DEAD;
         }
         if (threadIdx.x == 0) flag = 0;
         __syncthreads();
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
+        if (wid == 0) {
             uint32_t cur = 0;
             int64_t ent = -1;
 #pragma unroll 1
@@ -399,35 +489,45 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
                 const bool pass = (i + 1 < k) && t == (int32_t)(i + 1);
                 const uint32_t nb = __ballot_sync(FULL, !pass);
                 const int js = nb ? __ffs(nb) - 1 : 32;
-                if (lane <= js && i < k)
-                    en[i] = lane == 0 ? ent : w.midx[f + i - 1];
+                if (lane <= js && i < k) en[i] = lane == 0 ? ent : mi[i - 1];
                 if (js == 32) {
-                    ent = w.midx[f + cur + 31];
+                    ent = mi[cur + 31];
                     cur += 32;
                     continue;
                 }
                 const uint32_t ic = cur + js;
-                if (ic + 1 == k) break;               // stream's last segment ends at E
+                if (ic + 1 == k) break;               // the stream's last segment ends at E
                 const int32_t tj = tg[ic];
                 if (tj == TGT_END) break;
                 if (tj < 0) {                         // overflow (or never set)
                     if (lane == 0) flag = 1;
                     break;
                 }
-                ent = w.midx[f + ic];
+                ent = mi[ic];
                 cur = (uint32_t)tj;
             }
         }
         __syncthreads();
         if (flag) {
+            // pathological stream: one warp re-walks it end to end into FB
             for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
                 w.seg_count[f + i] = 0;
                 w.entry[f + i] = ENTRY_DEAD;
             }
-            if (threadIdx.x == 0) {
-                w.str_flag[j] = 1;
-                w.flagged[atomicAdd(w.ctrl + C_NFLAG, 1u)] = j;
+            __syncthreads();
+            if (wid == 0) {
+                Walker wk;
+                walker_init(wk, sm, lane);
+                const uint64_t S0 = w.single ? 0 : w.offs[j], E = w.single ? w.total : w.offs[j + 1];
+                const uint64_t o0 = w.single ? 0 : w.offs[0];
+                const uint32_t n = fallback_stream<MODE, LONG>(w, wk, S0, E, w.FB + (S0 - o0) / w.p.mn + j, lane);
+                if (lane == 0) {
+                    w.seg_count[f] = n;
+                    w.entry[f] = ENTRY_DEAD;
+                }
             }
+            if (threadIdx.x == 0 && !w.single) w.str_flag[j] = 1;
+            if (threadIdx.x == 0 && w.single) w.ctrl[C_NFLAG] = 1;
         } else {
             for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
                 const int64_t e = en[i];
@@ -436,56 +536,24 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
                 w.seg_count[f + i] = c;
                 w.entry[f + i] = e;
             }
-            if (threadIdx.x == 0) w.str_flag[j] = 0;
+            if (threadIdx.x == 0 && !w.single) w.str_flag[j] = 0;
         }
         __syncthreads();
     }
-}
-
-// ------------------------------------------------------------------ 4. fallback (rare)
-template <int MODE, bool SMALL_M>
-__global__ void __launch_bounds__(32) k_fallback(Work w)
-{
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int lane = threadIdx.x;
-    if (w.ctrl[C_BAD] || w.ctrl[C_NFLAG] == 0) return;
-    Ring rg;
-    rg.buf = smem_u32(smem);
-    rg.bar = smem_u32(smem + RING);
-    rg.pending = 0;
-    rg.nextpar = 0;
-    rg.t_first = rg.t_next = rg.t_end = 0;
-    rg.a_lo = rg.a_hi = 0;
-    if (lane < STAGES) mbar_init(rg.bar + 8 * lane, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-    const uint64_t abase = (uint64_t)(uintptr_t)w.in;
-    const uint32_t nflag = w.ctrl[C_NFLAG];
-#pragma unroll 1
-    for (;;) {
-        uint32_t q = 0;
-        if (lane == 0) q = atomicAdd(w.ctrl + C_NEXT_FB, 1u);
-        q = __shfl_sync(FULL, q, 0);
-        if (q >= nflag) break;
-        const uint32_t j = w.flagged[q];
-        const uint64_t S0 = w.offs[j], E = w.offs[j + 1];
-        uint64_t *dst = w.FB + (S0 - w.offs[0]) / w.p.mn + j;
-        ring_start(rg, abase + S0, abase + E, abase + S0);
-        ListBuf lb{0, 0};
-        uint64_t base = abase + S0;
-#pragma unroll 1
-        while (base < abase + E) {
-            const uint64_t cut = resolve_chunk<MODE, SMALL_M>(rg, w.p, base, abase + E, lane);
-            lb_push(lb, cut - abase, dst, lane);
-            base = cut;
+    if (w.single && blockIdx.x == 0) {
+        __syncthreads();
+        const uint64_t total = block_scan(
+            w.nseg1, [&](uint64_t s) -> uint64_t { return w.seg_count[s]; },
+            [&](uint64_t s, uint64_t ex) { w.seg_out[s] = ex; });
+        if (threadIdx.x == 0) {
+            w.cut_index[0] = 0;
+            w.cut_index[1] = total;
+            *w.ncuts = total;
         }
-        lb_flush(lb, dst, lane);
-        if (lane == 0) w.seg_count[w.str_first[j]] = lb.n;
     }
-    ring_drain(rg);
 }
 
-// ------------------------------------------------------------------ 5. scan, 6. copy
+// ------------------------------------------------------------------ 3. scan (batches), 4. copy
 __global__ void __launch_bounds__(1024) k_scan(Work w)
 {
     if (w.ctrl[C_BAD]) {
@@ -507,27 +575,28 @@ __global__ void __launch_bounds__(1024) k_scan(Work w)
 __global__ void __launch_bounds__(256) k_copy(Work w)
 {
     if (w.ctrl[C_BAD]) return;
-    const uint32_t nseg = w.ctrl[C_NSEG];
+    const uint32_t nseg = nseg_total(w);
     const int lane = threadIdx.x & 31;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
     for (uint32_t s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nseg; s += warps) {
-        const uint32_t j = w.seg_stream[s];
-        uint64_t *out = w.cuts + w.seg_out[s];
-        if (w.str_flag[j]) {
-            if (s != w.str_first[j]) continue;
-            const uint64_t *src = w.FB + (w.offs[j] - w.offs[0]) / w.p.mn + j;
-            const uint64_t n = w.seg_count[s];
-            for (uint64_t i = lane; i < n; i += 32) out[i] = src[i];
+        const int64_t e = w.entry[s];
+        const uint64_t lc = w.Lcnt[s] & CNT_MASK, nx = w.Xcnt[s], o = w.seg_out[s], cnt = w.seg_count[s];
+        uint64_t *out = w.cuts + o;
+        const Seg g = get_seg(w, s);
+        const bool flagged = w.single ? (w.ctrl[C_NFLAG] != 0) : (w.str_flag[g.j] != 0);
+        if (flagged) {
+            if (s != g.first) continue;
+            const uint64_t o0 = w.single ? 0 : w.offs[0];
+            const uint64_t *src = w.FB + (g.S0 - o0) / w.p.mn + g.j;
+            for (uint64_t i = lane; i < cnt; i += 32) out[i] = src[i];
             continue;
         }
-        const int64_t e = w.entry[s];
         if (e == ENTRY_DEAD) continue;
-        const uint64_t nl = (w.Lcnt[s] & CNT_MASK) - (uint64_t)(e + 1);
-        const uint64_t *Ls = w.L + w.Loff[s] + (e + 1);
-        for (uint64_t i = lane; i < nl; i += 32) out[i] = Ls[i];
-        const uint64_t nx = w.Xcnt[s];
-        const uint64_t *Xs = w.X + w.Xoff[s];
-        for (uint64_t i = lane; i < nx; i += 32) out[nl + i] = Xs[i];
+        const uint64_t nl = lc - (uint64_t)(e + 1);
+        const uint64_t *Ls = w.L + g.Loff + (e + 1);
+        for (uint64_t i = lane; i < nl; i += 32) out[i] = __ldcg(Ls + i);
+        const uint64_t *Xs = w.X + g.Xoff;
+        for (uint64_t i = lane; i < nx; i += 32) out[nl + i] = __ldcg(Xs + i);
     }
 }
 
@@ -537,12 +606,19 @@ __global__ void k_empty(uint64_t *cut_index, uint64_t *ncuts)
     *ncuts = 0;
 }
 
+__global__ void k_single_offsets(uint64_t *offs, uint64_t n)
+{
+    offs[0] = 0;
+    offs[1] = n;
+}
+
 // ------------------------------------------------------------------ host side
 struct Plan {
     uint64_t G, nseg_max, L_items, X_items, FB_items;
+    uint32_t nseg1, capL1, capX1;
     size_t bytes;
-    size_t o_ctrl, o_str_first, o_str_flag, o_flagged, o_seg_lo, o_seg_hi, o_seg_stream, o_Loff, o_Xoff,
-        o_Lcap, o_Xcap, o_Lcnt, o_Xcnt, o_target, o_midx, o_entry, o_seg_count, o_seg_out, o_L, o_X, o_FB;
+    size_t o_ctrl, o_Lcnt, o_str_first, o_str_flag, o_seg_lo, o_seg_hi, o_seg_stream, o_Loff, o_Xoff,
+        o_Lcap, o_Xcap, o_Xcnt, o_target, o_midx, o_entry, o_seg_count, o_seg_out, o_L, o_X, o_FB;
     uint32_t walk_grid;
 };
 
@@ -552,31 +628,35 @@ static std::mutex g_mu;
 static cudaMemPool_t g_pool[64];
 static bool g_pool_ok[64];
 
+template <int MODE, bool LONG>
+static void set_attrs()
+{
+    cudaFuncSetAttribute((const void *)k_walk<MODE, LONG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_WALK);
+    cudaFuncSetAttribute((const void *)k_stitch<MODE, LONG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_WALK + 20 * STITCH_MAX_SEGS);
+}
+
 static int device_info(int &sms, int &occ)
 {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_sms) {
         int dev;
         if (cudaGetDevice(&dev) != cudaSuccess) return SEQCDC_ECUDA;
-        if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            return SEQCDC_ECUDA;
-        const int smem = RING + STAGES * 8;
-        auto set_attrs = [&](const void *fn) {
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        };
-        set_attrs((const void *)k_walk<0, true>);
-        set_attrs((const void *)k_walk<1, true>);
-        set_attrs((const void *)k_walk<0, false>);
-        set_attrs((const void *)k_walk<1, false>);
-        set_attrs((const void *)k_fallback<0, true>);
-        set_attrs((const void *)k_fallback<1, true>);
-        set_attrs((const void *)k_fallback<0, false>);
-        set_attrs((const void *)k_fallback<1, false>);
-        cudaFuncSetAttribute((const void *)k_stitch, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        int nsm = 0;
+        if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return SEQCDC_ECUDA;
+        set_attrs<0, false>();
+        set_attrs<0, true>();
+        set_attrs<1, false>();
+        set_attrs<1, true>();
         int occ_ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, true>, 32, smem) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, false>, 32, SMEM_WALK) != cudaSuccess)
             return SEQCDC_ECUDA;
+        if (const char *e = getenv("SEQCDC_WALKERS_PER_SM")) {
+            int v = atoi(e);
+            if (v > 0 && v < occ_) occ_ = v;
+        }
         g_occ = occ_ > 0 ? occ_ : 1;
+        g_sms = nsm;
     }
     sms = g_sms;
     occ = g_occ;
@@ -585,20 +665,33 @@ static int device_info(int &sms, int &occ)
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int sms, int occ, Plan &pl)
+static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int sms, int occ, Plan &pl,
+                      bool single)
 {
     const uint64_t walkers = (uint64_t)sms * occ;
+    const uint64_t mx = p->max_size, mn = p->min_size;
     uint64_t denom = walkers > 2ull * ns ? walkers - ns : std::max<uint64_t>(walkers / 2, 1);
     uint64_t G = (total + denom - 1) / denom;
-    G = std::max<uint64_t>(G, G_FLOOR_CHUNKS * p->max_size);
-    if (g_force_G) G = std::max<uint64_t>(g_force_G, p->max_size);
-    G = (G + p->max_size - 1) / p->max_size * p->max_size;
+    G = std::max<uint64_t>(G, G_FLOOR_CHUNKS * mx);
+    if (g_force_G) G = std::max<uint64_t>(g_force_G, mx);
+    G = std::min<uint64_t>(G, std::max<uint64_t>(G_CEIL, mx));
+    G = (G + mx - 1) / mx * mx;
     pl.G = G;
-    pl.nseg_max = (uint64_t)ns + total / G + 1;
-    pl.L_items = total / p->min_size + 2 * pl.nseg_max + 2;
-    pl.X_items = K_EXT * (total / p->min_size) + 2 * pl.nseg_max + 2;
-    pl.FB_items = total / p->min_size + ns + 2;
-    pl.walk_grid = (uint32_t)std::min<uint64_t>(pl.nseg_max, walkers);
+    if (single) {
+        pl.nseg1 = (uint32_t)(total <= G ? 1 : (total + G - 1) / G);
+        pl.nseg_max = pl.nseg1;
+        pl.capL1 = (uint32_t)(G / mn + 2);
+        pl.capX1 = (uint32_t)(std::min<uint64_t>(K_EXT * G, total) / mn + 2);
+        pl.L_items = (uint64_t)pl.nseg1 * pl.capL1;
+        pl.X_items = (uint64_t)pl.nseg1 * pl.capX1;
+    } else {
+        pl.nseg1 = pl.capL1 = pl.capX1 = 0;
+        pl.nseg_max = (uint64_t)ns + total / G + 1;
+        pl.L_items = total / mn + 2 * pl.nseg_max + 2;
+        pl.X_items = K_EXT * (total / mn) + 2 * pl.nseg_max + 2;
+    }
+    pl.FB_items = total / mn + ns + 2;
+    pl.walk_grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(pl.nseg_max, walkers));
     size_t o = 0;
     auto take = [&](size_t bytes) {
         size_t r = o;
@@ -607,17 +700,17 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     };
     const uint64_t S = pl.nseg_max;
     pl.o_ctrl = take(C_NWORDS * 4);
+    pl.o_Lcnt = o;  // contiguous with ctrl: one memset resets both
+    o = align_up(o + 8 * S, 256);
     pl.o_str_first = take(4ull * (ns + 1));
     pl.o_str_flag = take(4ull * ns);
-    pl.o_flagged = take(4ull * ns);
-    pl.o_seg_lo = take(8 * S);
-    pl.o_seg_hi = take(8 * S);
-    pl.o_seg_stream = take(4 * S);
-    pl.o_Loff = take(8 * S);
-    pl.o_Xoff = take(8 * S);
-    pl.o_Lcap = take(4 * S);
-    pl.o_Xcap = take(4 * S);
-    pl.o_Lcnt = take(8 * S);
+    pl.o_seg_lo = take(single ? 0 : 8 * S);
+    pl.o_seg_hi = take(single ? 0 : 8 * S);
+    pl.o_seg_stream = take(single ? 0 : 4 * S);
+    pl.o_Loff = take(single ? 0 : 8 * S);
+    pl.o_Xoff = take(single ? 0 : 8 * S);
+    pl.o_Lcap = take(single ? 0 : 4 * S);
+    pl.o_Xcap = take(single ? 0 : 4 * S);
     pl.o_Xcnt = take(4 * S);
     pl.o_target = take(4 * S);
     pl.o_midx = take(8 * S);
@@ -651,41 +744,45 @@ static int get_pool(cudaMemPool_t &pool)
     return SEQCDC_OK;
 }
 
-template <int MODE, bool SMALL_M>
-static void launch_walkers(const Work &w, const Plan &pl, int sms, cudaStream_t st)
+// ------------------------------------------------------------------ profiling (bench only)
+// When enabled, every call records 4 events on its stream: before the reset,
+// before the walk, after the walk, after the copy.  collect() sums elapsed times.
+struct ProfRec { cudaEvent_t e[4]; };
+static bool g_prof = false;
+static std::vector<ProfRec> g_prof_recs;
+
+static void prof_mark(ProfRec *r, int i, cudaStream_t st)
 {
-    const int smem = RING + STAGES * 8;
-    k_walk<MODE, SMALL_M><<<pl.walk_grid, 32, smem, st>>>(w);
-    const uint64_t kmax = std::min<uint64_t>(pl.nseg_max, w.total / pl.G + 2);
-    k_stitch<<<std::min<uint64_t>(w.ns, 4ull * sms), 1024, (size_t)(kmax * 12 + 32), st>>>(w);
-    k_fallback<MODE, SMALL_M><<<sms, 32, smem, st>>>(w);
+    if (r) cudaEventRecord(r->e[i], st);
+}
+
+template <int MODE, bool LONG>
+static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
+{
+    prof_mark(pr, 1, st);
+    k_walk<MODE, LONG><<<pl.walk_grid, 32, SMEM_WALK, st>>>(w);
+    prof_mark(pr, 2, st);
+    const uint32_t sgrid = w.single ? 1u : (uint32_t)std::min<uint64_t>(w.ns, 2ull * sms);
+    k_stitch<MODE, LONG><<<sgrid, 1024, SMEM_WALK + 20 * STITCH_MAX_SEGS, st>>>(w);
+    if (!w.single) k_scan<<<1, 1024, 0, st>>>(w);
+    k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
 }
 
 static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total,
                const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index, uint64_t *d_ncuts,
-               void *d_ws, size_t ws_bytes, cudaStream_t st)
+               uint8_t *ws, size_t ws_bytes, const Plan &pl, int sms, cudaStream_t st, bool single)
 {
-    int sms, occ;
-    int rc = device_info(sms, occ);
-    if (rc) return rc;
-    Plan pl;
-    make_plan(total, ns, p, sms, occ, pl);
-    if (total / pl.G + 2 > 15000) return SEQCDC_EINVAL;  // stitch keeps one stream's segments in smem
-    uint8_t *ws = (uint8_t *)d_ws;
-    bool owned = false;
-    if (ws) {
-        if (ws_bytes < pl.bytes) return SEQCDC_ENOMEM;
-    } else {
-        cudaMemPool_t pool;
-        if ((rc = get_pool(pool))) return rc;
-        if (cudaMallocFromPoolAsync((void **)&ws, pl.bytes, pool, st) != cudaSuccess) return SEQCDC_ENOMEM;
-        owned = true;
-    }
+    if (ws_bytes < pl.bytes) return SEQCDC_ENOMEM;
+    if (total / pl.G + 2 > STITCH_MAX_SEGS) return SEQCDC_EINVAL;  // one stream's segments fit the stitch smem
     Work w;
     memset(&w, 0, sizeof(w));
     w.in = d_in;
     w.offs = d_offsets;
     w.ns = ns;
+    w.single = single ? 1u : 0u;
+    w.nseg1 = pl.nseg1;
+    w.capL1 = pl.capL1;
+    w.capX1 = pl.capX1;
     w.G = pl.G;
     w.total = total;
     w.p.L = p->seq_length;
@@ -695,9 +792,9 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.p.mn = p->min_size;
     w.p.mx = p->max_size;
     w.ctrl = (uint32_t *)(ws + pl.o_ctrl);
+    w.Lcnt = (uint64_t *)(ws + pl.o_Lcnt);
     w.str_first = (uint32_t *)(ws + pl.o_str_first);
     w.str_flag = (uint32_t *)(ws + pl.o_str_flag);
-    w.flagged = (uint32_t *)(ws + pl.o_flagged);
     w.seg_lo = (uint64_t *)(ws + pl.o_seg_lo);
     w.seg_hi = (uint64_t *)(ws + pl.o_seg_hi);
     w.seg_stream = (uint32_t *)(ws + pl.o_seg_stream);
@@ -705,7 +802,6 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.Xoff = (uint64_t *)(ws + pl.o_Xoff);
     w.Lcap = (uint32_t *)(ws + pl.o_Lcap);
     w.Xcap = (uint32_t *)(ws + pl.o_Xcap);
-    w.Lcnt = (uint64_t *)(ws + pl.o_Lcnt);
     w.Xcnt = (uint32_t *)(ws + pl.o_Xcnt);
     w.target = (int32_t *)(ws + pl.o_target);
     w.midx = (int64_t *)(ws + pl.o_midx);
@@ -719,16 +815,68 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.cut_index = d_cut_index;
     w.ncuts = d_ncuts;
 
-    k_setup<<<1, 1024, 0, st>>>(w);
-    const bool small = p->seq_length <= 5;
-    if (p->mode == SEQCDC_INCREASING) {
-        if (small) launch_walkers<0, true>(w, pl, sms, st); else launch_walkers<0, false>(w, pl, sms, st);
-    } else {
-        if (small) launch_walkers<1, true>(w, pl, sms, st); else launch_walkers<1, false>(w, pl, sms, st);
+    ProfRec rec, *pr = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (g_prof) {
+            for (int i = 0; i < 4; i++) cudaEventCreate(&rec.e[i]);
+            pr = &rec;
+        }
     }
-    k_scan<<<1, 1024, 0, st>>>(w);
-    k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
-    rc = cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
+    prof_mark(pr, 0, st);
+    if (w.single) {
+        if (cudaMemsetAsync(ws + pl.o_ctrl, 0, pl.o_Lcnt - pl.o_ctrl + 8 * pl.nseg1, st) != cudaSuccess)
+            return SEQCDC_ECUDA;
+    } else {
+        k_setup<<<1, 1024, 0, st>>>(w);
+    }
+    const bool lng = p->seq_length > 5;
+    const int key = (p->mode == SEQCDC_INCREASING ? 0 : 2) + (lng ? 1 : 0);
+    switch (key) {
+    case 0: launch_all<0, false>(w, pl, sms, st, pr); break;
+    case 1: launch_all<0, true>(w, pl, sms, st, pr); break;
+    case 2: launch_all<1, false>(w, pl, sms, st, pr); break;
+    default: launch_all<1, true>(w, pl, sms, st, pr); break;
+    }
+    prof_mark(pr, 3, st);
+    if (pr) {
+        std::lock_guard<std::mutex> lk(g_mu);
+        g_prof_recs.push_back(rec);
+    }
+    return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
+}
+
+// single-stream calls keep their [0, n] offsets and cut index in front of the workspace
+constexpr size_t SINGLE_EXTRA = 256;
+
+static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total,
+                   const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index, uint64_t *d_ncuts,
+                   void *d_ws, size_t ws_bytes, cudaStream_t st, bool single_api)
+{
+    int sms, occ;
+    int rc = device_info(sms, occ);
+    if (rc) return rc;
+    Plan pl;
+    make_plan(total, ns, p, sms, occ, pl, single_api);
+    const size_t extra = single_api ? SINGLE_EXTRA : 0;
+    uint8_t *ws = (uint8_t *)d_ws;
+    bool owned = false;
+    if (ws) {
+        if (ws_bytes < pl.bytes + extra) return SEQCDC_ENOMEM;
+    } else {
+        cudaMemPool_t pool;
+        if ((rc = get_pool(pool))) return rc;
+        if (cudaMallocFromPoolAsync((void **)&ws, pl.bytes + extra, pool, st) != cudaSuccess) return SEQCDC_ENOMEM;
+        owned = true;
+    }
+    if (single_api) {
+        uint64_t *offs = (uint64_t *)ws;
+        d_offsets = offs;
+        d_cut_index = offs + 2;
+        k_single_offsets<<<1, 1, 0, st>>>(offs, total);
+    }
+    rc = run(d_in, d_offsets, ns, total, p, d_cuts, d_cut_index, d_ncuts, ws + extra, pl.bytes, pl, sms, st,
+             single_api);
     if (owned) cudaFreeAsync(ws, st);
     return rc;
 }
@@ -745,7 +893,7 @@ SEQCDC_API int seqcdc_validate_params(const seqcdc_params_t *p)
     if (p->skip_trigger < 1) return SEQCDC_EINVAL;
     if (p->min_size < p->seq_length) return SEQCDC_EINVAL;
     if (p->max_size < p->min_size) return SEQCDC_EINVAL;
-    if (p->max_size > (1ull << 40)) return SEQCDC_EINVAL;
+    if (p->max_size > (1ull << 28)) return SEQCDC_EINVAL;  // implementation limit: 256 MiB chunks
     if (p->flags || p->reserved) return SEQCDC_EINVAL;
     return SEQCDC_OK;
 }
@@ -753,14 +901,14 @@ SEQCDC_API int seqcdc_validate_params(const seqcdc_params_t *p)
 SEQCDC_API int seqcdc_default_params(uint32_t avg_kib, uint32_t mode, seqcdc_params_t *out)
 {
     if (!out || mode > 1) return SEQCDC_EINVAL;
-    uint32_t L = 5, T, S;
+    uint32_t T, S;
     if (avg_kib == 4) { T = 55; S = 256; }
     else if (avg_kib == 8) { T = 50; S = 256; }
     else if (avg_kib == 16) { T = 50; S = 512; }
     else return SEQCDC_EINVAL;
     memset(out, 0, sizeof(*out));
     out->mode = mode;
-    out->seq_length = L;
+    out->seq_length = 5;
     out->skip_trigger = T;
     out->skip_size = S;
     out->min_size = (uint64_t)avg_kib * 512;
@@ -786,17 +934,18 @@ SEQCDC_API size_t seqcdc_workspace_size(uint64_t total, uint32_t ns, const seqcd
     int sms, occ;
     if (device_info(sms, occ)) {
         sms = 148;
-        occ = 16;
+        occ = 32;
     }
     Plan pl;
-    make_plan(total, ns ? ns : 1, p, sms, occ, pl);
-    return pl.bytes + 256;  // + the offsets slice seqcdc_chunk() keeps in front
+    Plan pb;
+    make_plan(total, ns ? ns : 1, p, sms, occ, pl, ns <= 1);
+    make_plan(total, ns ? ns : 1, p, sms, occ, pb, false);
+    return std::max(pl.bytes, pb.bytes) + SINGLE_EXTRA;
 }
 
-SEQCDC_API int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns,
-                                  uint64_t total, const seqcdc_params_t *p, uint64_t *d_cuts,
-                                  uint64_t *d_cut_index, uint64_t *d_ncuts, void *d_ws, size_t ws_bytes,
-                                  void *stream)
+SEQCDC_API int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total,
+                                  const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index,
+                                  uint64_t *d_ncuts, void *d_ws, size_t ws_bytes, void *stream)
 {
     if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
     if (!d_offsets || !d_cut_index || !d_ncuts) return SEQCDC_EINVAL;
@@ -806,16 +955,8 @@ SEQCDC_API int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets
         k_empty<<<1, 1, 0, st>>>(d_cut_index, d_ncuts);
         return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
     }
-    return run(d_in, d_offsets, ns, total, p, d_cuts, d_cut_index, d_ncuts, d_ws, ws_bytes, st);
+    return enqueue(d_in, d_offsets, ns, total, p, d_cuts, d_cut_index, d_ncuts, d_ws, ws_bytes, st, false);
 }
-
-namespace seqcdc {
-__global__ void k_single_offsets(uint64_t *offs, uint64_t n)
-{
-    offs[0] = 0;
-    offs[1] = n;
-}
-}  // namespace seqcdc
 
 SEQCDC_API int seqcdc_chunk(const uint8_t *d_in, uint64_t n, const seqcdc_params_t *p, uint64_t *d_cuts,
                             uint64_t *d_ncuts, void *d_ws, size_t ws_bytes, void *stream)
@@ -823,35 +964,46 @@ SEQCDC_API int seqcdc_chunk(const uint8_t *d_in, uint64_t n, const seqcdc_params
     if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
     if (!d_ncuts) return SEQCDC_EINVAL;
     if (n && (!d_in || !d_cuts)) return SEQCDC_EINVAL;
-    cudaStream_t st = (cudaStream_t)stream;
-    // offsets[2] + cut_index[2] live in a small extra workspace slice
-    int sms, occ;
-    int rc = device_info(sms, occ);
-    if (rc) return rc;
-    Plan pl;
-    make_plan(n, 1, p, sms, occ, pl);
-    const size_t extra = 256;
-    uint8_t *ws = (uint8_t *)d_ws;
-    bool owned = false;
-    if (ws) {
-        if (ws_bytes < pl.bytes + extra) return SEQCDC_ENOMEM;
-    } else {
-        cudaMemPool_t pool;
-        if ((rc = get_pool(pool))) return rc;
-        if (cudaMallocFromPoolAsync((void **)&ws, pl.bytes + extra, pool, st) != cudaSuccess)
-            return SEQCDC_ENOMEM;
-        owned = true;
+    return enqueue(d_in, nullptr, 1, n, p, d_cuts, nullptr, d_ncuts, d_ws, ws_bytes, (cudaStream_t)stream, true);
+}
+
+SEQCDC_API int seqcdc_profile_enable(int on)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto &r : g_prof_recs)
+        for (int i = 0; i < 4; i++) cudaEventDestroy(r.e[i]);
+    g_prof_recs.clear();
+    g_prof = on != 0;
+    return SEQCDC_OK;
+}
+
+SEQCDC_API int seqcdc_profile_collect(double *ms, uint64_t *ncalls)
+{
+    std::lock_guard<std::mutex> lk(g_mu);
+    double acc[4] = {0, 0, 0, 0};
+    for (auto &r : g_prof_recs) {
+        if (cudaEventSynchronize(r.e[3]) != cudaSuccess) return SEQCDC_ECUDA;
+        float t;
+        cudaEventElapsedTime(&t, r.e[0], r.e[1]);
+        acc[0] += t;
+        cudaEventElapsedTime(&t, r.e[1], r.e[2]);
+        acc[1] += t;
+        cudaEventElapsedTime(&t, r.e[2], r.e[3]);
+        acc[2] += t;
+        cudaEventElapsedTime(&t, r.e[0], r.e[3]);
+        acc[3] += t;
+        for (int i = 0; i < 4; i++) cudaEventDestroy(r.e[i]);
     }
-    uint64_t *offs = (uint64_t *)ws;
-    uint64_t *cidx = offs + 2;
-    k_single_offsets<<<1, 1, 0, st>>>(offs, n);
-    rc = run(d_in, offs, 1, n, p, d_cuts, cidx, d_ncuts, ws + extra, pl.bytes, st);
-    if (owned) cudaFreeAsync(ws, st);
-    return rc;
+    if (ms)
+        for (int i = 0; i < 4; i++) ms[i] = acc[i];
+    if (ncalls) *ncalls = g_prof_recs.size();
+    g_prof_recs.clear();
+    return SEQCDC_OK;
 }
 
 SEQCDC_API int seqcdc_set_segment_bytes(uint64_t g)
 {
+    std::lock_guard<std::mutex> lk(g_mu);
     g_force_G = g;
     return SEQCDC_OK;
 }
@@ -869,8 +1021,10 @@ SEQCDC_API const char *seqcdc_strerror(int code)
 
 SEQCDC_API const char *seqcdc_build_info(void)
 {
-    static char buf[160];
-    snprintf(buf, sizeof(buf), "seqcdc sm_100a tile=%u stages=%d ring=%u win_pairs=%u k_ext=%u", TILE, STAGES,
-             RING, WIN_PAIRS, K_EXT);
+    static char buf[192];
+    int sms = 0, occ = 0;
+    device_info(sms, occ);
+    snprintf(buf, sizeof(buf), "seqcdc sm_100a tile=%u stages=%d ring=%u win_pairs=%u k_ext=%u walkers=%dx%d",
+             TILE, STAGES, RING, WIN_PAIRS, K_EXT, sms, occ);
     return buf;
 }
