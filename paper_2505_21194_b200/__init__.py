@@ -72,8 +72,8 @@ def lib():
     """Load libseqcdc.so (building it in-tree first if sources are newer)."""
     global _lib
     if _lib is None:
-        path = _build.LIB
-        if _build.stale():
+        path = os.environ.get("SEQCDC_LIB") or _build.LIB   # SEQCDC_LIB: tuning variants only
+        if path == _build.LIB and _build.stale():
             path = _build.build()
         if not os.path.exists(path):
             raise SeqCDCError(f"libseqcdc.so missing at {path}; run __graft_entry__.build()")

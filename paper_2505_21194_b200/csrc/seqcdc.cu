@@ -38,6 +38,9 @@
 #include "seqcdc_device.cuh"
 
 #define SEQCDC_API extern "C" __attribute__((visibility("default")))
+#ifndef SEQCDC_MIN_BLOCKS
+#define SEQCDC_MIN_BLOCKS 1
+#endif
 
 namespace seqcdc {
 
@@ -48,7 +51,7 @@ constexpr int32_t TGT_OVERFLOW = -3;
 constexpr int64_t ENTRY_DEAD = -2;
 constexpr uint32_t K_EXT = 4;             // extension budget, in segments
 constexpr uint64_t G_FLOOR_CHUNKS = 32;   // minimum segment length, in max_size units
-constexpr uint64_t G_CEIL = 256ull << 20; // keeps a chain's span far below REBASE_AT
+constexpr uint64_t G_CEIL = 64ull << 20;  // keeps a chain's span (G + K_EXT*G + max) far below REL_CLAMP
 constexpr uint32_t STITCH_MAX_SEGS = 8000;
 
 enum { C_NSEG = 0, C_NEXT = 1, C_NFLAG = 2, C_BAD = 3, C_NWORDS = 8 };
@@ -318,52 +321,42 @@ __device__ int check_cut(const Work &w, Cursor &c, uint32_t t, uint64_t t_lo, ui
     }
 }
 
-__device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, int lane)
-{
-    wk.buf = smem_u32(smem);
-    wk.bar = smem_u32(smem + RING);
-    wk.pending = 0;
-    wk.nextpar = 0;
-    wk.rb = 0;
-    wk.lo_rel = wk.end_rel = 0;
-    wk.t_first = wk.t_next = wk.t_end = 0;
-    wk.res_lo = wk.res_hi = 0;
-    if (lane < STAGES) mbar_init(wk.bar + 8 * lane, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-}
-
-template <int MODE, bool LONG>
+template <int MODE, int MSPEC>
 __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
 {
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
     const Seg g = get_seg(w, s);
-    const uint64_t Eabs = abase + g.E;
-    uint32_t base = walker_start(wk, abase + g.lo, Eabs);
+    uint32_t base = walker_begin(wk, abase + g.lo, abase + g.E, lane);
+    const uint64_t off = wk.rb - abase;                      // relative position -> offset into `in`
+    const uint32_t end_rel = wk.end_rel;
+    const uint32_t hi_rel = g.last ? FULL : base + (uint32_t)(g.hi - g.lo);
     uint64_t *Ls = w.L + g.Loff;
     ListBuf lb{0, 0};
-    uint64_t cut = 0;      // offset into `in` of the latest cut
+    uint32_t c = base;
     bool extend = false;
     // spec phase: cuts < hi belong to L_s
-    const uint64_t hi_abs = abase + g.hi;
 #pragma unroll 1
-    while (wk.rb + base < Eabs) {
-        base = walker_rebase(wk, base, Eabs);
-        const uint32_t c = resolve<MODE, LONG>(wk, w.p, base, lane);
-        const uint64_t cabs = wk.rb + c;
-        cut = cabs - abase;
-        if (!g.last && cabs >= hi_abs) {
+    while (base < end_rel) {
+        c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+        if (c >= hi_rel) {
             extend = true;
-            base = c;
             break;
         }
-        lb_push(lb, cut, Ls, lane);
+        lb_push(lb, off + c, Ls, lane);
         if ((lb.n & 31) == 0) publish(w.Lcnt + s, lb.n, false, lane);
         base = c;
     }
     lb_flush(lb, Ls, lane);
     publish(w.Lcnt + s, lb.n, true, lane);
-    if (!extend) return;
+    if (!extend) {                       // the stream's last segment: no extension
+        if (lane == 0) {
+            w.Xcnt[s] = 0;
+            w.target[s] = TGT_END;
+            w.midx[s] = -1;
+        }
+        walker_end(wk, lane);
+        return;
+    }
 
     // ---- extension: walk on until a cut coincides with the chain owning it
     uint64_t *Xs = w.X + g.Xoff;
@@ -372,12 +365,14 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
     int32_t tgt = TGT_OVERFLOW;
     int64_t mi = -1;
     uint64_t t_lo = 0, t_Loff = 0;
+    const uint32_t ext_end = hi_rel + (uint32_t)(K_EXT * w.G);  // byte budget (REL_CLAMP safety)
 #pragma unroll 1
     for (;;) {
-        if (xb.n == g.Xcap) {
+        if (xb.n == g.Xcap || c > ext_end) {
             tgt = TGT_OVERFLOW;
             break;
         }
+        const uint64_t cut = off + c;
         lb_push(xb, cut, Xs, lane);
         if (cut == g.E) {
             tgt = TGT_END;
@@ -394,10 +389,8 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
             mi = idx;
             break;
         }
-        base = walker_rebase(wk, base, Eabs);
-        const uint32_t c = resolve<MODE, LONG>(wk, w.p, base, lane);
-        cut = wk.rb + c - abase;
         base = c;
+        c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
     }
     lb_flush(xb, Xs, lane);
     if (lane == 0) {
@@ -405,50 +398,62 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
         w.target[s] = tgt;
         w.midx[s] = mi;
     }
+    walker_end(wk, lane);
 }
 
-template <int MODE, bool LONG>
-__global__ void __launch_bounds__(32) k_walk(Work w)
+// One CTA = one walker warp (warp 0) + one TMA producer warp (warp 1).
+template <int MODE, int MSPEC>
+__global__ void __launch_bounds__(PAIR_THREADS, SEQCDC_MIN_BLOCKS) k_walk(Work w)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    RingCtl *ctl = pair_init(smem, tid);
+    if (tid >= 32) {
+        producer_loop(smem, ctl, lane);
+        return;
+    }
     Walker wk;
-    walker_init(wk, smem, lane);
-    if (w.ctrl[C_BAD]) return;
-    const uint32_t nseg = nseg_total(w);
+    walker_init(wk, smem, ctl);
+    const uint32_t nseg = w.ctrl[C_BAD] ? 0u : nseg_total(w);
 #pragma unroll 1
     for (;;) {
         uint32_t s = 0;
         if (lane == 0) s = atomicAdd(w.ctrl + C_NEXT, 1u);
         s = __shfl_sync(FULL, s, 0);
         if (s >= nseg) break;
-        walk_segment<MODE, LONG>(w, wk, s, lane);
+        walk_segment<MODE, MSPEC>(w, wk, s, lane);
     }
-    ring_drain(wk);
+    walker_quit(wk, lane);
 }
 
 // ------------------------------------------------------------------ 2. stitch (+fallback, +scan for one stream)
-// One warp re-walks a whole stream (used only when an extension overflowed).
-template <int MODE, bool LONG>
+// One walker/producer pair re-walks a whole stream (only when an extension
+// overflowed), in jobs of <= 1 GiB so relative positions stay 32-bit.
+template <int MODE, int MSPEC>
 __device__ uint32_t fallback_stream(const Work &w, Walker &wk, uint64_t S0, uint64_t E, uint64_t *dst, int lane)
 {
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
-    const uint64_t Eabs = abase + E;
-    uint32_t base = walker_start(wk, abase + S0, Eabs);
     ListBuf lb{0, 0};
+    uint64_t pos = S0;                   // offset of the current chunk start
 #pragma unroll 1
-    while (wk.rb + base < Eabs) {
-        base = walker_rebase(wk, base, Eabs);
-        const uint32_t c = resolve<MODE, LONG>(wk, w.p, base, lane);
-        lb_push(lb, wk.rb + c - abase, dst, lane);
-        base = c;
+    while (pos < E) {
+        uint32_t base = walker_begin(wk, abase + pos, abase + E, lane);
+        const uint64_t off = wk.rb - abase;
+        const uint32_t stop_at = base + REBASE_AT;
+#pragma unroll 1
+        while (base < wk.end_rel && base < stop_at) {
+            const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+            lb_push(lb, off + c, dst, lane);
+            base = c;
+        }
+        pos = off + base;
+        walker_end(wk, lane);
     }
     lb_flush(lb, dst, lane);
-    ring_drain(wk);
     return lb.n;
 }
 
-template <int MODE, bool LONG>
+template <int MODE, int MSPEC>
 __global__ void __launch_bounds__(1024) k_stitch(Work w)
 {
     extern __shared__ __align__(128) uint8_t sm[];
@@ -515,15 +520,22 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
                 w.entry[f + i] = ENTRY_DEAD;
             }
             __syncthreads();
-            if (wid == 0) {
-                Walker wk;
-                walker_init(wk, sm, lane);
-                const uint64_t S0 = w.single ? 0 : w.offs[j], E = w.single ? w.total : w.offs[j + 1];
-                const uint64_t o0 = w.single ? 0 : w.offs[0];
-                const uint32_t n = fallback_stream<MODE, LONG>(w, wk, S0, E, w.FB + (S0 - o0) / w.p.mn + j, lane);
-                if (lane == 0) {
-                    w.seg_count[f] = n;
-                    w.entry[f] = ENTRY_DEAD;
+            if (wid < 2) {
+                RingCtl *ctl = pair_init(sm, threadIdx.x);
+                if (wid == 1) {
+                    producer_loop(sm, ctl, lane);
+                } else {
+                    Walker wk;
+                    walker_init(wk, sm, ctl);
+                    const uint64_t S0 = w.single ? 0 : w.offs[j], E = w.single ? w.total : w.offs[j + 1];
+                    const uint64_t o0 = w.single ? 0 : w.offs[0];
+                    const uint32_t n =
+                        fallback_stream<MODE, MSPEC>(w, wk, S0, E, w.FB + (S0 - o0) / w.p.mn + j, lane);
+                    walker_quit(wk, lane);
+                    if (lane == 0) {
+                        w.seg_count[f] = n;
+                        w.entry[f] = ENTRY_DEAD;
+                    }
                 }
             }
             if (threadIdx.x == 0 && !w.single) w.str_flag[j] = 1;
@@ -628,11 +640,11 @@ static std::mutex g_mu;
 static cudaMemPool_t g_pool[64];
 static bool g_pool_ok[64];
 
-template <int MODE, bool LONG>
+template <int MODE, int MSPEC>
 static void set_attrs()
 {
-    cudaFuncSetAttribute((const void *)k_walk<MODE, LONG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_WALK);
-    cudaFuncSetAttribute((const void *)k_stitch<MODE, LONG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute((const void *)k_walk<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_WALK);
+    cudaFuncSetAttribute((const void *)k_stitch<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SMEM_WALK + 20 * STITCH_MAX_SEGS);
 }
 
@@ -644,12 +656,14 @@ static int device_info(int &sms, int &occ)
         if (cudaGetDevice(&dev) != cudaSuccess) return SEQCDC_ECUDA;
         int nsm = 0;
         if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return SEQCDC_ECUDA;
-        set_attrs<0, false>();
-        set_attrs<0, true>();
-        set_attrs<1, false>();
-        set_attrs<1, true>();
+        set_attrs<0, 4>();
+        set_attrs<0, 0>();
+        set_attrs<0, -1>();
+        set_attrs<1, 4>();
+        set_attrs<1, 0>();
+        set_attrs<1, -1>();
         int occ_ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, false>, 32, SMEM_WALK) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4>, PAIR_THREADS, SMEM_WALK) != cudaSuccess)
             return SEQCDC_ECUDA;
         if (const char *e = getenv("SEQCDC_WALKERS_PER_SM")) {
             int v = atoi(e);
@@ -756,14 +770,14 @@ static void prof_mark(ProfRec *r, int i, cudaStream_t st)
     if (r) cudaEventRecord(r->e[i], st);
 }
 
-template <int MODE, bool LONG>
+template <int MODE, int MSPEC>
 static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
 {
     prof_mark(pr, 1, st);
-    k_walk<MODE, LONG><<<pl.walk_grid, 32, SMEM_WALK, st>>>(w);
+    k_walk<MODE, MSPEC><<<pl.walk_grid, PAIR_THREADS, SMEM_WALK, st>>>(w);
     prof_mark(pr, 2, st);
     const uint32_t sgrid = w.single ? 1u : (uint32_t)std::min<uint64_t>(w.ns, 2ull * sms);
-    k_stitch<MODE, LONG><<<sgrid, 1024, SMEM_WALK + 20 * STITCH_MAX_SEGS, st>>>(w);
+    k_stitch<MODE, MSPEC><<<sgrid, 1024, SMEM_WALK + 20 * STITCH_MAX_SEGS, st>>>(w);
     if (!w.single) k_scan<<<1, 1024, 0, st>>>(w);
     k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
 }
@@ -830,13 +844,15 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     } else {
         k_setup<<<1, 1024, 0, st>>>(w);
     }
-    const bool lng = p->seq_length > 5;
-    const int key = (p->mode == SEQCDC_INCREASING ? 0 : 2) + (lng ? 1 : 0);
-    switch (key) {
-    case 0: launch_all<0, false>(w, pl, sms, st, pr); break;
-    case 1: launch_all<0, true>(w, pl, sms, st, pr); break;
-    case 2: launch_all<1, false>(w, pl, sms, st, pr); break;
-    default: launch_all<1, true>(w, pl, sms, st, pr); break;
+    const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
+    if (p->mode == SEQCDC_INCREASING) {
+        if (ms == 4) launch_all<0, 4>(w, pl, sms, st, pr);
+        else if (ms == 0) launch_all<0, 0>(w, pl, sms, st, pr);
+        else launch_all<0, -1>(w, pl, sms, st, pr);
+    } else {
+        if (ms == 4) launch_all<1, 4>(w, pl, sms, st, pr);
+        else if (ms == 0) launch_all<1, 0>(w, pl, sms, st, pr);
+        else launch_all<1, -1>(w, pl, sms, st, pr);
     }
     prof_mark(pr, 3, st);
     if (pr) {

@@ -49,7 +49,6 @@ constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint32_t H = 0x80808080u;
 constexpr uint32_t REL_CLAMP = 0xC0000000u;          // relative positions stay below this
 constexpr uint32_t REBASE_AT = 0x40000000u;          // rebase a chain past 1 GiB
-constexpr uint32_t SMEM_WALK = RING + STAGES * 8;    // dynamic smem of one walker
 
 struct DevParams {
     uint32_t L, T, S, M;   // M = L-1 favourable pairs per run
@@ -148,177 +147,337 @@ __device__ __forceinline__ void lt_gt_flags(uint32_t x, uint32_t y, uint32_t &lt
     gt = (~y & x) | (~(x ^ y) & u);
 }
 
-// ------------------------------------------------------------------ one walker (warp-uniform state)
+// ------------------------------------------------------------------ walker / producer pair
+// Each CTA runs one chain with two warps: warp 0 walks (consumer), warp 1 is
+// the TMA producer.  The producer streams the job's tiles in order into a
+// STAGES-slot ring: tile t goes to slot t % STAGES, completion on full[slot]
+// (arrive.expect_tx + cp.async.bulk).  The walker waits on full[] in tile
+// order and releases each tile (arrive on empty[slot]) only after it waited
+// for it, so every wait targets the slot's next fill (no phase ambiguity);
+// the producer reuses a slot once empty[] shows the previous tile released.
+// Fill sequence numbers g run on across jobs; the relative origin rb of a job
+// is chosen so that slot(tile) == g % STAGES.
+struct RingCtl {                 // in shared memory, after the ring
+    uint64_t full[STAGES];
+    uint64_t empty[STAGES];
+    uint64_t rb;                 // job: absolute address of relative 0
+    uint32_t lo_rel, end_rel;    // job: loadable relative byte range
+    uint32_t t0, t_end;          // job: first / one-past-last tile
+    uint32_t g0;                 // job: fill sequence number of tile t0
+    volatile uint32_t stop;      // walker -> producer: job finished
+    uint32_t g_next;             // producer -> walker: sequence after the last issued fill
+    uint32_t quit;               // walker -> producer: no more jobs
+};
+constexpr uint32_t LOG_STAGES = STAGES == 2 ? 1 : STAGES == 4 ? 2 : STAGES == 8 ? 3 : 4;
+constexpr uint32_t SMEM_WALK = RING + ((sizeof(RingCtl) + 127) & ~127u);  // dynamic smem of one pair
+constexpr int PAIR_THREADS = 64;
+constexpr int PAIR_BARRIER = 1;                                           // named barrier id
+
+__device__ __forceinline__ void pair_sync()
+{
+    asm volatile("bar.sync %0, %1;" ::"n"(PAIR_BARRIER), "n"(PAIR_THREADS) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// try_wait with a suspend-time hint: the waiting thread sleeps (no issue
+// slots) until the phase completes or ~hint ns pass.
+__device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(1000u)
+        : "memory");
+    return ok != 0;
+}
+
 struct Walker {
-    uint64_t rb;        // absolute address of relative position 0 (RING-aligned)
+    uint64_t rb;        // absolute address of relative position 0
     uint32_t lo_rel;    // first loadable byte (relative)
     uint32_t end_rel;   // end of the stream (relative, clamped to REL_CLAMP)
-    uint32_t buf, bar;  // shared addresses: ring, mbarriers
-    uint32_t t_first;   // oldest tile still owned (relative tile index)
-    uint32_t t_next;    // next tile to issue
-    uint32_t t_end;     // one past the last tile with data
-    uint32_t res_lo, res_hi;  // byte range known resident (all tiles waited)
-    uint32_t pending;   // bit s: slot s holds an issued fill not yet waited for
-    uint32_t nextpar;   // bit s: parity of the slot's next fill
+    uint32_t buf;       // shared address of the ring
+    uint32_t full, empty;  // shared addresses of the barrier arrays
+    RingCtl *ctl;
+    uint32_t t0, g0;    // first tile of the job and its fill sequence number
+    uint32_t t_rel;     // next tile to release
+    uint32_t t_wait;    // next tile to wait for (all tiles below were waited)
+    uint32_t res_lo, res_hi;  // byte range resident: tiles [res_lo, res_hi) waited, not released
+    uint32_t g;         // fill sequence number after the last job
 };
 
-__device__ __forceinline__ void ring_wait_slot(Walker &wk, uint32_t s)
+__device__ __forceinline__ uint32_t tile_parity(const Walker &wk, uint32_t t)
 {
-    if (wk.pending & (1u << s)) {
-        mbar_wait(wk.bar + 8 * s, ((wk.nextpar >> s) & 1u) ^ 1u);
-        wk.pending &= ~(1u << s);
-    }
+    return ((wk.g0 + (t - wk.t0)) >> LOG_STAGES) & 1u;
 }
 
-__device__ __forceinline__ void ring_drain(Walker &wk)
+// Both warps: set up the ring and barriers of a pair whose smem starts at `smem`.
+__device__ __forceinline__ RingCtl *pair_init(uint8_t *smem, int tid)
 {
-#pragma unroll
-    for (uint32_t s = 0; s < (uint32_t)STAGES; s++) ring_wait_slot(wk, s);
+    RingCtl *ctl = (RingCtl *)(smem + RING);
+    if (tid < STAGES) {
+        mbar_init(smem_u32(&ctl->full[tid]), 1);
+        mbar_init(smem_u32(&ctl->empty[tid]), 1);
+    }
+    if (tid == 0) {
+        ctl->stop = 0;
+        ctl->quit = 0;
+        ctl->g_next = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    pair_sync();
+    return ctl;
 }
 
-// Issue relative tile t (warp-uniform).  TMA moves the 16-byte-aligned
-// interior; lanes copy the <16-byte ragged head/tail of the loadable range.
-__device__ __forceinline__ void ring_issue(Walker &wk, uint32_t t, int lane)
+__device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, RingCtl *ctl)
 {
-    const uint32_t s = t & (STAGES - 1);
-    ring_wait_slot(wk, s);  // never two fills in flight on one slot
-    uint32_t lo = t << TILE_SHIFT, hi = lo + TILE;
-    if (lo < wk.lo_rel) lo = wk.lo_rel;
-    if (hi > wk.end_rel) hi = wk.end_rel;
-    const uint32_t mlo = (lo + 15) & ~15u, mhi = hi & ~15u;
-    uint32_t tx = 0;
-    if (lo < hi && mlo < mhi) tx = mhi - mlo;
-    const uint32_t bar = wk.bar + 8 * s;
-    if (lane == 0) {
-        mbar_arrive_tx(bar, tx);
-        if (tx) tma_load_1d(wk.buf + (mlo & RING_MASK), (const void *)(wk.rb + mlo), tx, bar);
-    }
-    if (lo < hi && (lo != mlo || hi != mhi || !tx)) {
-        uint32_t pos;
-        bool ok;
-        if (tx) {
-            pos = lane < 16 ? lo + lane : mhi + (lane - 16);
-            ok = lane < 16 ? pos < mlo : pos < hi;
-        } else {
-            pos = lo + lane;
-            ok = pos < hi;
-        }
-        if (ok) sts8(wk.buf + (pos & RING_MASK), *(const volatile uint8_t *)(wk.rb + pos));
-        __syncwarp();
-    }
-    wk.pending |= 1u << s;
-    wk.nextpar ^= 1u << s;
-}
-
-// Slow path of ring_ensure: release tiles below need_lo, top up the ring,
-// wait for the tiles covering [need_lo, need_hi).
-__device__ __forceinline__ void ring_refill(Walker &wk, uint32_t need_lo, uint32_t need_hi, int lane)
-{
-    const uint32_t tlo = need_lo >> TILE_SHIFT, thi = (need_hi - 1) >> TILE_SHIFT;
-    if (tlo > wk.t_first) {
-        wk.t_first = tlo;
-        if (wk.t_next < tlo) wk.t_next = tlo;
-    }
-#pragma unroll 1
-    while (wk.t_next < wk.t_end && wk.t_next < wk.t_first + STAGES) {
-        ring_issue(wk, wk.t_next, lane);
-        wk.t_next++;
-    }
-    ring_wait_slot(wk, tlo & (STAGES - 1));
-    if (thi != tlo) ring_wait_slot(wk, thi & (STAGES - 1));
-    wk.res_lo = tlo << TILE_SHIFT;
-    wk.res_hi = (thi + 1) << TILE_SHIFT;
-}
-
-__device__ __forceinline__ void ring_ensure(Walker &wk, uint32_t need_lo, uint32_t need_hi, int lane)
-{
-    if (need_lo < wk.res_lo || need_hi > wk.res_hi) ring_refill(wk, need_lo, need_hi, lane);
-}
-
-// Start a chain whose loadable data is absolute [a_lo, a_end); returns the
-// relative position of a_lo.
-__device__ __forceinline__ uint32_t walker_start(Walker &wk, uint64_t a_lo, uint64_t a_end)
-{
-    ring_drain(wk);
-    wk.rb = a_lo & ~(uint64_t)RING_MASK;
-    wk.lo_rel = (uint32_t)(a_lo - wk.rb);
-    const uint64_t e = a_end - wk.rb;
-    wk.end_rel = e > REL_CLAMP ? REL_CLAMP : (uint32_t)e;
-    wk.t_end = wk.end_rel > 0 ? ((wk.end_rel - 1) >> TILE_SHIFT) + 1 : 0;
-    wk.t_first = wk.t_next = wk.lo_rel >> TILE_SHIFT;
+    wk.buf = smem_u32(smem);
+    wk.ctl = ctl;
+    wk.full = smem_u32(&ctl->full[0]);
+    wk.empty = smem_u32(&ctl->empty[0]);
+    wk.g = 0;
+    wk.rb = 0;
+    wk.lo_rel = wk.end_rel = 0;
+    wk.t0 = wk.g0 = wk.t_rel = wk.t_wait = 0;
     wk.res_lo = wk.res_hi = 0;
+}
+
+// Walker: start a job whose loadable data is absolute [a_lo, a_end); returns
+// the relative position of a_lo.  Pairs with the producer's job wait.
+__device__ __forceinline__ uint32_t walker_begin(Walker &wk, uint64_t a_lo, uint64_t a_end, int lane)
+{
+    const uint32_t k = wk.g & (STAGES - 1);
+    wk.rb = (a_lo & ~(uint64_t)(TILE - 1)) - (uint64_t)k * TILE;
+    wk.lo_rel = (uint32_t)(a_lo - wk.rb);
+    const uint64_t e = a_end > a_lo ? a_end - wk.rb : wk.lo_rel;
+    wk.end_rel = e > REL_CLAMP ? REL_CLAMP : (uint32_t)e;
+    wk.t0 = k;
+    wk.g0 = wk.g;
+    wk.t_rel = wk.t_wait = k;
+    wk.res_lo = wk.res_hi = 0;
+    if (lane == 0) {
+        RingCtl *c = wk.ctl;
+        c->rb = wk.rb;
+        c->lo_rel = wk.lo_rel;
+        c->end_rel = wk.end_rel;
+        c->t0 = k;
+        c->t_end = wk.end_rel > wk.lo_rel ? ((wk.end_rel - 1) >> TILE_SHIFT) + 1 : k;
+        c->g0 = wk.g;
+        c->stop = 0;
+        c->quit = 0;
+    }
+    pair_sync();   // job visible to the producer
     return wk.lo_rel;
 }
 
-// Move the relative origin forward so that `pos` stays small (only at chunk
-// boundaries; keeps tile numbering consistent: shift is a RING multiple).
-__device__ __forceinline__ uint32_t walker_rebase(Walker &wk, uint32_t pos, uint64_t a_end)
+__device__ __forceinline__ void walker_wait_tile(Walker &wk, uint32_t t)
 {
-    if (pos < REBASE_AT) return pos;
-    ring_drain(wk);
-    const uint32_t sh = (pos - RING) & ~RING_MASK;
-    wk.rb += sh;
-    wk.lo_rel = 0;
-    const uint64_t e = a_end - wk.rb;
-    wk.end_rel = e > REL_CLAMP ? REL_CLAMP : (uint32_t)e;
-    wk.t_end = wk.end_rel > 0 ? ((wk.end_rel - 1) >> TILE_SHIFT) + 1 : 0;
-    const uint32_t np = pos - sh;
-    wk.t_first = wk.t_next = np >> TILE_SHIFT;
-    wk.res_lo = wk.res_hi = 0;
-    return np;
+    mbar_wait(wk.full + 8 * (t & (STAGES - 1)), tile_parity(wk, t));
+}
+
+__device__ __forceinline__ void walker_release_tile(Walker &wk, uint32_t t, int lane)
+{
+    if (lane == 0) mbar_arrive(wk.empty + 8 * (t & (STAGES - 1)));
+}
+
+// Walker slow path: make bytes [need_lo, need_hi) resident (need_hi-need_lo <= TILE);
+// tiles below need_lo are released (after being waited, in order).
+__device__ __forceinline__ void walker_need(Walker &wk, uint32_t need_lo, uint32_t need_hi, int lane)
+{
+    const uint32_t tlo = need_lo >> TILE_SHIFT, thi = (need_hi - 1) >> TILE_SHIFT;
+#pragma unroll 1
+    for (uint32_t t = wk.t_wait; t <= thi; t++) {
+#pragma unroll 1
+        while (wk.t_rel < tlo && wk.t_rel + STAGES <= t) {
+            walker_release_tile(wk, wk.t_rel, lane);
+            wk.t_rel++;
+        }
+        walker_wait_tile(wk, t);
+    }
+    if (wk.t_wait <= thi) wk.t_wait = thi + 1;
+#pragma unroll 1
+    while (wk.t_rel < tlo) {
+        walker_release_tile(wk, wk.t_rel, lane);
+        wk.t_rel++;
+    }
+    wk.res_lo = tlo << TILE_SHIFT;
+    wk.res_hi = wk.t_wait << TILE_SHIFT;
+}
+
+// Walker: finish the job (producer stops; every issued tile waited + released).
+__device__ __forceinline__ void walker_end(Walker &wk, int lane)
+{
+    if (lane == 0) wk.ctl->stop = 1;
+    pair_sync();   // producer has stopped and published g_next
+    const uint32_t gn = wk.ctl->g_next;
+    const uint32_t t_hi = wk.t0 + (gn - wk.g0);
+#pragma unroll 1
+    for (uint32_t t = wk.t_wait; t < t_hi; t++) walker_wait_tile(wk, t);
+    if (wk.t_wait < t_hi) wk.t_wait = t_hi;
+#pragma unroll 1
+    for (uint32_t t = wk.t_rel; t < t_hi; t++) walker_release_tile(wk, t, lane);
+    wk.t_rel = t_hi;
+    wk.g = gn;
+    __syncwarp();
+}
+
+// Walker: no more jobs.
+__device__ __forceinline__ void walker_quit(Walker &wk, int lane)
+{
+    if (lane == 0) wk.ctl->quit = 1;
+    pair_sync();
+}
+
+// Producer warp: serve jobs until the walker quits.
+__device__ __noinline__ void producer_loop(uint8_t *smem, RingCtl *ctl, int lane)
+{
+    const uint32_t buf = smem_u32(smem);
+    const uint32_t full = smem_u32(&ctl->full[0]), empty = smem_u32(&ctl->empty[0]);
+#pragma unroll 1
+    for (;;) {
+        pair_sync();                       // job posted (or quit)
+        if (ctl->quit) break;
+        const uint64_t rb = ctl->rb;
+        const uint32_t lo_rel = ctl->lo_rel, end_rel = ctl->end_rel, t_end = ctl->t_end;
+        uint32_t t = ctl->t0, g = ctl->g0;
+#pragma unroll 1
+        for (; t < t_end; t++, g++) {
+            const uint32_t s = t & (STAGES - 1);
+            if (g >= (uint32_t)STAGES) {   // slot reuse: the walker released the slot's previous tile
+                const uint32_t par = ((g >> LOG_STAGES) - 1) & 1u;
+                bool stopped = false;
+#pragma unroll 1
+                while (!mbar_try_sleep(empty + 8 * s, par)) {
+                    if (ctl->stop) {
+                        stopped = true;
+                        break;
+                    }
+                }
+                if (stopped) break;
+            }
+            if (ctl->stop) break;
+            const uint32_t bar = full + 8 * s;
+            uint32_t lo = t << TILE_SHIFT, hi = lo + TILE;
+            if (lo >= lo_rel && hi <= end_rel) {
+                if (lane == 0) {
+                    mbar_arrive_tx(bar, TILE);
+                    tma_load_1d(buf + s * TILE, (const void *)(rb + lo), TILE, bar);
+                }
+            } else {
+                if (lo < lo_rel) lo = lo_rel;
+                if (hi > end_rel) hi = end_rel;
+                const uint32_t mlo = (lo + 15) & ~15u, mhi = hi & ~15u;
+                const uint32_t tx = (lo < hi && mlo < mhi) ? mhi - mlo : 0;
+                if (lo < hi) {   // ragged head/tail bytes by lanes, before the arrive
+                    uint32_t pos;
+                    bool ok;
+                    if (tx) {
+                        pos = lane < 16 ? lo + lane : mhi + (lane - 16);
+                        ok = lane < 16 ? pos < mlo : pos < hi;
+                    } else {
+                        pos = lo + lane;
+                        ok = pos < hi;
+                    }
+                    if (ok) sts8(buf + (pos & RING_MASK), *(const volatile uint8_t *)(rb + pos));
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive_tx(bar, tx);
+                    if (tx) tma_load_1d(buf + (mlo & RING_MASK), (const void *)(rb + mlo), tx, bar);
+                }
+            }
+        }
+        if (lane == 0) ctl->g_next = g;
+        pair_sync();                       // job finished (pairs with walker_end)
+    }
 }
 
 // ------------------------------------------------------------------ one chunk
+// Favourable-run mask R for M = L-1 pairs.  MSPEC = 4: exactly four (L = 5,
+// Table I); MSPEC = 0: any M <= 4 (runtime); MSPEC = -1: 5 <= M <= 15, using up
+// to four words back (the previous window's words arrive by shuffles).
+template <int MSPEC>
+__device__ __forceinline__ uint32_t run_mask(uint32_t Fm, uint32_t carry1, uint32_t prevwin, uint32_t M, int lane)
+{
+    if (MSPEC >= 0) {
+        const uint32_t up = __shfl_up_sync(FULL, Fm, 1);
+        const uint32_t W1 = lane ? up : carry1;
+        if (MSPEC == 4)
+            return Fm & __funnelshift_l(W1, Fm, 8) & __funnelshift_l(W1, Fm, 16) & __funnelshift_l(W1, Fm, 24);
+        uint32_t R = Fm;
+        if (M > 1) R &= __funnelshift_l(W1, Fm, 8);
+        if (M > 2) R &= __funnelshift_l(W1, Fm, 16);
+        if (M > 3) R &= __funnelshift_l(W1, Fm, 24);
+        return R;
+    } else {
+        uint32_t Wd[5];
+        Wd[0] = Fm;
+#pragma unroll
+        for (int k = 1; k <= 4; k++) {
+            const uint32_t a1 = __shfl_sync(FULL, Fm, (lane - k) & 31);
+            const uint32_t b1 = __shfl_sync(FULL, prevwin, (lane - k) & 31);
+            Wd[k] = lane >= k ? a1 : b1;
+        }
+        uint32_t R = Fm;
+#pragma unroll
+        for (uint32_t j = 1; j < 16; j++)
+            if (j < M) R &= __funnelshift_l(Wd[(j >> 2) + 1], Wd[j >> 2], 8 * (j & 3));
+        return R;
+    }
+}
+
 // f(base): the cut ending the chunk that starts at relative position `base`.
 // Warp-uniform; every lane returns the same value.
-template <int MODE>
+template <int MODE, int MSPEC>
 __device__ __forceinline__ uint32_t resolve_chunk(Walker &wk, const DevParams &p, uint32_t base, int lane)
 {
     const uint64_t lim64 = (uint64_t)base + p.mx;
     const uint32_t limit = lim64 < wk.end_rel ? (uint32_t)lim64 : wk.end_rel;
     if (limit - base < 2) return limit;
     const uint32_t lim2 = limit - 2;               // last pair that may be examined
-    uint32_t a = base + (uint32_t)p.mn - p.L;      // P:179 (mn - L < max <= 2^40 checked on host)
     if ((uint64_t)base + p.mn - p.L > lim2) return limit;
-    uint32_t oc = 0;                               // opposing pairs counted since the anchor a
-    uint32_t carry = 0;                            // previous window's lane-31 masked F word
+    uint32_t a = base + (uint32_t)p.mn - p.L;      // P:179
+    uint32_t need = p.T;                           // opposing pairs still needed for a skip
+    uint32_t carry = 0;                            // previous window's masked F (lane 31 / per lane)
     uint32_t p0 = a & ~3u;
-    uint32_t ra = a & 3u;                          // pairs of lane 0 below the anchor (first window)
+    uint32_t lomask = FULL << (8 * (a & 3u));      // lane 0: pairs below the anchor
     const uint32_t lt_mask = lanemask_lt();
+    const uint32_t qoff = 4 * (uint32_t)lane;
 #pragma unroll 1
     for (;;) {
-        uint32_t need_hi = p0 + WIN_PAIRS + 4;
-        if (need_hi > lim2 + 2) need_hi = lim2 + 2;
-        ring_ensure(wk, p0, need_hi, lane);
-        const uint32_t q = p0 + 4 * (uint32_t)lane;
+        if (p0 < wk.res_lo || p0 + (WIN_PAIRS + 4) > wk.res_hi) {
+            uint32_t need_hi = p0 + WIN_PAIRS + 4;
+            if (need_hi > lim2 + 2) need_hi = lim2 + 2;
+            if (p0 < wk.res_lo || need_hi > wk.res_hi) walker_need(wk, p0, need_hi, lane);
+        }
+        const uint32_t q = p0 + qoff;
         const uint32_t x = lds32(wk.buf + (q & RING_MASK));
         const uint32_t xn = lds32(wk.buf + ((q + 4) & RING_MASK));
         const uint32_t y = __funnelshift_r(x, xn, 8);     // y_k = byte q+k+1
         uint32_t lt, gt;
         lt_gt_flags(x, y, lt, gt);
-        // valid pairs: a <= pair <= lim2
-        const uint32_t rh = lim2 - p0 > 255u ? 255u : lim2 - p0;
-        const int32_t sh = 32 * lane + 24 - 8 * (int32_t)rh;
-        const uint32_t V = shl_c(FULL, lane ? 0u : 8u * ra) & shr_c(FULL, sh > 0 ? (uint32_t)sh : 0u) & H;
+        uint32_t V = (lane ? FULL : lomask) & H;
+        if (p0 + (WIN_PAIRS - 1) > lim2) {                // window crosses the last pair
+            const int32_t sh = (int32_t)qoff * 8 + 24 - 8 * (int32_t)(lim2 - p0);
+            V &= shr_c(FULL, sh > 0 ? (uint32_t)sh : 0u);
+        }
         const uint32_t Fm = (MODE == 0 ? lt : gt) & V;
         const uint32_t Om = (MODE == 0 ? gt : lt) & V;
-        // runs of M favourable pairs ending at each pair (M <= 4 here; longer
-        // runs are handled by resolve_chunk_long)
-        const uint32_t up = __shfl_up_sync(FULL, Fm, 1);
-        const uint32_t W1 = lane ? up : carry;
-        uint32_t R = Fm;
-        if (p.M > 1) R &= __funnelshift_l(W1, Fm, 8);
-        if (p.M > 2) R &= __funnelshift_l(W1, Fm, 16);
-        if (p.M > 3) R &= __funnelshift_l(W1, Fm, 24);
+        const uint32_t R = run_mask<MSPEC>(Fm, carry, carry, p.M, lane);
         const uint32_t rmask = __ballot_sync(FULL, R != 0);
         const uint32_t cnt = __popc(Om);
         const uint32_t total = __reduce_add_sync(FULL, cnt);
-        const uint32_t need = p.T - oc;
         if (rmask == 0 && total < need) {          // nothing decided in this window
-            oc += total;
-            carry = __shfl_sync(FULL, Fm, 31);
+            need -= total;
+            carry = MSPEC >= 0 ? __shfl_sync(FULL, Fm, 31) : Fm;
             p0 += WIN_PAIRS;
-            ra = 0;
+            lomask = FULL;
             if (p0 > lim2) return limit;
             continue;
         }
@@ -334,7 +493,7 @@ __device__ __forceinline__ uint32_t resolve_chunk(Walker &wk, const DevParams &p
                            b2 = __ballot_sync(FULL, cnt & 4);
             const uint32_t excl = __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask);
             const int dl = __ffs(__ballot_sync(FULL, excl + cnt >= need)) - 1;
-            // in lane dl: the k-th flag (k = need - excl); byte j holds flags of bytes 0..j
+            // in lane dl: the k-th flag (k = need - excl); byte j of pc = flags in bytes 0..j
             const uint32_t k = need - excl;
             const uint32_t pc = (Om >> 7) * 0x01010101u;
             const uint32_t ge = ((pc | H) - k * 0x01010101u) & 0x00808080u;
@@ -344,100 +503,17 @@ __device__ __forceinline__ uint32_t resolve_chunk(Walker &wk, const DevParams &p
         if (r < d) return r + 2;                   // boundary after the run
         if (p.S >= lim2 - d) return limit;         // skip lands past the last pair (c8)
         a = d + 1 + p.S;                           // content-defined skip (c3)
-        oc = 0;
+        need = p.T;
         carry = 0;
         p0 = a & ~3u;
-        ra = a & 3u;
+        lomask = FULL << (8 * (a & 3u));
     }
 }
 
-// Same resolution for 5 < L <= 16: runs of up to 15 favourable pairs span up
-// to four words back; the previous window's words come in by shuffles.
-template <int MODE>
-__device__ __forceinline__ uint32_t resolve_chunk_long(Walker &wk, const DevParams &p, uint32_t base, int lane)
-{
-    const uint64_t lim64 = (uint64_t)base + p.mx;
-    const uint32_t limit = lim64 < wk.end_rel ? (uint32_t)lim64 : wk.end_rel;
-    if (limit - base < 2) return limit;
-    const uint32_t lim2 = limit - 2;
-    uint32_t a = base + (uint32_t)p.mn - p.L;
-    if ((uint64_t)base + p.mn - p.L > lim2) return limit;
-    uint32_t oc = 0;
-    uint32_t prevwin = 0;   // previous window's masked F word of this lane
-    uint32_t p0 = a & ~3u;
-    uint32_t ra = a & 3u;
-    const uint32_t lt_mask = lanemask_lt();
-#pragma unroll 1
-    for (;;) {
-        uint32_t need_hi = p0 + WIN_PAIRS + 4;
-        if (need_hi > lim2 + 2) need_hi = lim2 + 2;
-        ring_ensure(wk, p0, need_hi, lane);
-        const uint32_t q = p0 + 4 * (uint32_t)lane;
-        const uint32_t x = lds32(wk.buf + (q & RING_MASK));
-        const uint32_t xn = lds32(wk.buf + ((q + 4) & RING_MASK));
-        const uint32_t y = __funnelshift_r(x, xn, 8);
-        uint32_t lt, gt;
-        lt_gt_flags(x, y, lt, gt);
-        const uint32_t rh = lim2 - p0 > 255u ? 255u : lim2 - p0;
-        const int32_t sh = 32 * lane + 24 - 8 * (int32_t)rh;
-        const uint32_t V = shl_c(FULL, lane ? 0u : 8u * ra) & shr_c(FULL, sh > 0 ? (uint32_t)sh : 0u) & H;
-        const uint32_t Fm = (MODE == 0 ? lt : gt) & V;
-        const uint32_t Om = (MODE == 0 ? gt : lt) & V;
-        uint32_t Wd[5];
-        Wd[0] = Fm;
-#pragma unroll
-        for (int k = 1; k <= 4; k++) {
-            const uint32_t a1 = __shfl_sync(FULL, Fm, (lane - k) & 31);
-            const uint32_t b1 = __shfl_sync(FULL, prevwin, (lane - k) & 31);
-            Wd[k] = lane >= k ? a1 : b1;
-        }
-        uint32_t R = Fm;
-#pragma unroll
-        for (uint32_t j = 1; j < 16; j++)
-            if (j < p.M) R &= __funnelshift_l(Wd[(j >> 2) + 1], Wd[j >> 2], 8 * (j & 3));
-        const uint32_t rmask = __ballot_sync(FULL, R != 0);
-        const uint32_t cnt = __popc(Om);
-        const uint32_t total = __reduce_add_sync(FULL, cnt);
-        const uint32_t need = p.T - oc;
-        if (rmask == 0 && total < need) {
-            oc += total;
-            prevwin = Fm;
-            p0 += WIN_PAIRS;
-            ra = 0;
-            if (p0 > lim2) return limit;
-            continue;
-        }
-        uint32_t r = FULL, d = FULL;
-        if (rmask) {
-            const int rl = __ffs(rmask) - 1;
-            const uint32_t rbyte = (uint32_t)(__ffs(R) - 1) >> 3;
-            r = p0 + 4 * (uint32_t)rl + __shfl_sync(FULL, rbyte, rl);
-        }
-        if (total >= need) {
-            const uint32_t b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),
-                           b2 = __ballot_sync(FULL, cnt & 4);
-            const uint32_t excl = __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask);
-            const int dl = __ffs(__ballot_sync(FULL, excl + cnt >= need)) - 1;
-            const uint32_t k = need - excl;
-            const uint32_t pc = (Om >> 7) * 0x01010101u;
-            const uint32_t ge = ((pc | H) - k * 0x01010101u) & 0x00808080u;
-            const uint32_t dbyte = 3u - __popc(ge);
-            d = p0 + 4 * (uint32_t)dl + __shfl_sync(FULL, dbyte, dl);
-        }
-        if (r < d) return r + 2;
-        if (p.S >= lim2 - d) return limit;
-        a = d + 1 + p.S;
-        oc = 0;
-        prevwin = 0;
-        p0 = a & ~3u;
-        ra = a & 3u;
-    }
-}
-
-template <int MODE, bool LONG>
+template <int MODE, int MSPEC>
 __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint32_t base, int lane)
 {
-    return LONG ? resolve_chunk_long<MODE>(wk, p, base, lane) : resolve_chunk<MODE>(wk, p, base, lane);
+    return resolve_chunk<MODE, MSPEC>(wk, p, base, lane);
 }
 
 }  // namespace seqcdc
