@@ -326,7 +326,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
 {
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
     const Seg g = get_seg(w, s);
-    uint32_t base = walker_begin(wk, abase + g.lo, abase + g.E, lane);
+    uint32_t base = walker_begin(wk, abase + g.lo, abase + g.E);
     const uint64_t off = wk.rb - abase;                      // relative position -> offset into `in`
     const uint32_t end_rel = wk.end_rel;
     const uint32_t hi_rel = g.last ? FULL : base + (uint32_t)(g.hi - g.lo);
@@ -354,7 +354,6 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
             w.target[s] = TGT_END;
             w.midx[s] = -1;
         }
-        walker_end(wk, lane);
         return;
     }
 
@@ -398,22 +397,15 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
         w.target[s] = tgt;
         w.midx[s] = mi;
     }
-    walker_end(wk, lane);
 }
 
-// One CTA = one walker warp (warp 0) + one TMA producer warp (warp 1).
 template <int MODE, int MSPEC>
-__global__ void __launch_bounds__(PAIR_THREADS, SEQCDC_MIN_BLOCKS) k_walk(Work w)
+__global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
 {
     extern __shared__ __align__(128) uint8_t smem[];
-    const int tid = threadIdx.x, lane = tid & 31;
-    RingCtl *ctl = pair_init(smem, tid);
-    if (tid >= 32) {
-        producer_loop(smem, ctl, lane);
-        return;
-    }
+    const int lane = threadIdx.x;
     Walker wk;
-    walker_init(wk, smem, ctl);
+    walker_init(wk, smem);
     const uint32_t nseg = w.ctrl[C_BAD] ? 0u : nseg_total(w);
 #pragma unroll 1
     for (;;) {
@@ -423,12 +415,12 @@ __global__ void __launch_bounds__(PAIR_THREADS, SEQCDC_MIN_BLOCKS) k_walk(Work w
         if (s >= nseg) break;
         walk_segment<MODE, MSPEC>(w, wk, s, lane);
     }
-    walker_quit(wk, lane);
+    walker_finish(wk);
 }
 
 // ------------------------------------------------------------------ 2. stitch (+fallback, +scan for one stream)
-// One walker/producer pair re-walks a whole stream (only when an extension
-// overflowed), in jobs of <= 1 GiB so relative positions stay 32-bit.
+// One warp re-walks a whole stream (only when an extension overflowed), in
+// jobs of <= 1 GiB so relative positions stay 32-bit.
 template <int MODE, int MSPEC>
 __device__ uint32_t fallback_stream(const Work &w, Walker &wk, uint64_t S0, uint64_t E, uint64_t *dst, int lane)
 {
@@ -437,9 +429,9 @@ __device__ uint32_t fallback_stream(const Work &w, Walker &wk, uint64_t S0, uint
     uint64_t pos = S0;                   // offset of the current chunk start
 #pragma unroll 1
     while (pos < E) {
-        uint32_t base = walker_begin(wk, abase + pos, abase + E, lane);
+        uint32_t base = walker_begin(wk, abase + pos, abase + E);
         const uint64_t off = wk.rb - abase;
-        const uint32_t stop_at = base + REBASE_AT;
+        const uint32_t stop_at = base + JOB_SPAN;
 #pragma unroll 1
         while (base < wk.end_rel && base < stop_at) {
             const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
@@ -447,9 +439,9 @@ __device__ uint32_t fallback_stream(const Work &w, Walker &wk, uint64_t S0, uint
             base = c;
         }
         pos = off + base;
-        walker_end(wk, lane);
     }
     lb_flush(lb, dst, lane);
+    walker_finish(wk);
     return lb.n;
 }
 
@@ -520,22 +512,15 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
                 w.entry[f + i] = ENTRY_DEAD;
             }
             __syncthreads();
-            if (wid < 2) {
-                RingCtl *ctl = pair_init(sm, threadIdx.x);
-                if (wid == 1) {
-                    producer_loop(sm, ctl, lane);
-                } else {
-                    Walker wk;
-                    walker_init(wk, sm, ctl);
-                    const uint64_t S0 = w.single ? 0 : w.offs[j], E = w.single ? w.total : w.offs[j + 1];
-                    const uint64_t o0 = w.single ? 0 : w.offs[0];
-                    const uint32_t n =
-                        fallback_stream<MODE, MSPEC>(w, wk, S0, E, w.FB + (S0 - o0) / w.p.mn + j, lane);
-                    walker_quit(wk, lane);
-                    if (lane == 0) {
-                        w.seg_count[f] = n;
-                        w.entry[f] = ENTRY_DEAD;
-                    }
+            if (wid == 0) {
+                Walker wk;
+                walker_init(wk, sm);
+                const uint64_t S0 = w.single ? 0 : w.offs[j], E = w.single ? w.total : w.offs[j + 1];
+                const uint64_t o0 = w.single ? 0 : w.offs[0];
+                const uint32_t n = fallback_stream<MODE, MSPEC>(w, wk, S0, E, w.FB + (S0 - o0) / w.p.mn + j, lane);
+                if (lane == 0) {
+                    w.seg_count[f] = n;
+                    w.entry[f] = ENTRY_DEAD;
                 }
             }
             if (threadIdx.x == 0 && !w.single) w.str_flag[j] = 1;
@@ -663,7 +648,7 @@ static int device_info(int &sms, int &occ)
         set_attrs<1, 0>();
         set_attrs<1, -1>();
         int occ_ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4>, PAIR_THREADS, SMEM_WALK) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4>, 32, SMEM_WALK) != cudaSuccess)
             return SEQCDC_ECUDA;
         if (const char *e = getenv("SEQCDC_WALKERS_PER_SM")) {
             int v = atoi(e);
@@ -774,7 +759,7 @@ template <int MODE, int MSPEC>
 static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
 {
     prof_mark(pr, 1, st);
-    k_walk<MODE, MSPEC><<<pl.walk_grid, PAIR_THREADS, SMEM_WALK, st>>>(w);
+    k_walk<MODE, MSPEC><<<pl.walk_grid, 32, SMEM_WALK, st>>>(w);
     prof_mark(pr, 2, st);
     const uint32_t sgrid = w.single ? 1u : (uint32_t)std::min<uint64_t>(w.ns, 2ull * sms);
     k_stitch<MODE, MSPEC><<<sgrid, 1024, SMEM_WALK + 20 * STITCH_MAX_SEGS, st>>>(w);
@@ -803,8 +788,9 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.p.T = p->skip_trigger;
     w.p.S = p->skip_size;
     w.p.M = p->seq_length - 1;
-    w.p.mn = p->min_size;
-    w.p.mx = p->max_size;
+    w.p.mn = (uint32_t)p->min_size;
+    w.p.mx = (uint32_t)p->max_size;
+    w.p.mnL = (uint32_t)p->min_size - p->seq_length;
     w.ctrl = (uint32_t *)(ws + pl.o_ctrl);
     w.Lcnt = (uint64_t *)(ws + pl.o_Lcnt);
     w.str_first = (uint32_t *)(ws + pl.o_str_first);
@@ -1040,7 +1026,7 @@ SEQCDC_API const char *seqcdc_build_info(void)
     static char buf[192];
     int sms = 0, occ = 0;
     device_info(sms, occ);
-    snprintf(buf, sizeof(buf), "seqcdc sm_100a tile=%u stages=%d ring=%u win_pairs=%u k_ext=%u walkers=%dx%d",
-             TILE, STAGES, RING, WIN_PAIRS, K_EXT, sms, occ);
+    snprintf(buf, sizeof(buf), "seqcdc sm_100a blk=%u nblk=%u ahead=%u ring=%u win_pairs=%u k_ext=%u walkers=%dx%d",
+             BLK, NBLK, AHEAD, RING, WIN_PAIRS, K_EXT, sms, occ);
     return buf;
 }
