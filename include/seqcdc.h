@@ -128,6 +128,52 @@ int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t 
                        uint64_t *d_cuts, uint64_t *d_cut_index, uint64_t *d_ncuts,
                        void *d_workspace, size_t ws_bytes, void *stream);
 
+/*
+ * Range calls: the building blocks of the multi-GPU layer (one huge stream
+ * sharded over P ranks; paper_2505_21194_b200/dist.py).  A
+ * rank holds the range [R, R + range_len) of the stream in d_buf[0 ..
+ * range_len) followed by a right halo: d_buf[range_len .. buf_len) holds the
+ * next bytes of the stream.  buf_len is treated as the end of the stream, so
+ * a non-final range needs a halo of at least max_size - 1 bytes (then no
+ * chunk starting in the range sees it); the final range has buf_len ==
+ * range_len == the rest of the stream.  "The next cut depends only on the
+ * previous cut" (f(base) reads only [base, f(base)) and
+ * the stream end) is what makes a range chunkable before its true first
+ * chunk start is known.
+ *
+ * seqcdc_range_chunk: the chain of chunks that starts at local offset `entry`
+ * (as if a cut were there; 0 <= entry <= range_len), up to and including its
+ * first cut >= range_len (the "overhang": where the next range's first chunk
+ * starts) -- or the end of the stream.  Cuts are written as global offsets
+ * (global_offset + local).  entry == range_len gives 0 cuts.  d_cuts capacity:
+ * seqcdc_range_max_cuts(buf_len, range_len, p).  Workspace as for
+ * seqcdc_chunk.  Errors: SEQCDC_EINVAL (bad params, range_len > buf_len,
+ * entry > range_len, NULL pointers), SEQCDC_ENOMEM, SEQCDC_ECUDA.
+ */
+uint64_t seqcdc_range_max_cuts(uint64_t buf_len, uint64_t range_len, const seqcdc_params_t *p);
+int seqcdc_range_chunk(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                       uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
+                       uint64_t *d_ncuts, void *d_workspace, size_t ws_bytes, void *stream);
+
+/*
+ * seqcdc_range_resync: the TRUE chain of the range, given its true first
+ * chunk start `entry` (local; the previous range's overhang minus R) and a
+ * speculative chain d_spec[0 .. *d_spec_n) of the same range (global offsets,
+ * from seqcdc_range_chunk).  One warp re-walks from `entry` until a cut also
+ * present in d_spec (a merge: from there on both chains coincide) or until its
+ * first cut >= range_len.  Writes the true chain (re-walked prefix + reused
+ * speculative suffix) to d_cuts (capacity seqcdc_range_max_cuts; must not
+ * alias d_spec), its length to *d_ncuts, and d_status[4] = {merged (1/0),
+ * re-walked cuts, merge index in d_spec, overhang (global)}.  A range whose
+ * re-walk did not merge has a new overhang, which the next range must be
+ * re-synchronised from (dist.py repeats the exchange until nothing changes).
+ * Errors as for seqcdc_range_chunk.
+ */
+int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                        uint64_t global_offset, const seqcdc_params_t *p, const uint64_t *d_spec,
+                        const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
+                        uint64_t *d_status, void *stream);
+
 /* Testing / tuning knob: force the segment length G (rounded up to a
  * multiple of max_size, and to at least max_size) used to split streams into
  * speculative chains; 0 restores the automatic choice.  Process-global.  The

@@ -29,6 +29,7 @@ EXPORTS = (
     "seqcdc_validate_params", "seqcdc_default_params", "seqcdc_max_cuts", "seqcdc_max_cuts_batch",
     "seqcdc_workspace_size", "seqcdc_chunk", "seqcdc_chunk_batch", "seqcdc_strerror",
     "seqcdc_build_info", "seqcdc_set_segment_bytes", "seqcdc_profile_enable", "seqcdc_profile_collect",
+    "seqcdc_range_max_cuts", "seqcdc_range_chunk", "seqcdc_range_resync",
 )
 
 
@@ -104,13 +105,12 @@ def lib():
         L.seqcdc_profile_enable.restype = ctypes.c_int
         L.seqcdc_profile_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
         L.seqcdc_profile_collect.restype = ctypes.c_int
-        if hasattr(L, "seqcdc_range_chunk"):
-            L.seqcdc_range_chunk.argtypes = [p, u64, u64, u64, u64, u32, P, p, p, p, sz, p]
-            L.seqcdc_range_chunk.restype = ctypes.c_int
-            L.seqcdc_range_max_cuts.argtypes = [u64, u64, P]
-            L.seqcdc_range_max_cuts.restype = u64
-            L.seqcdc_range_finalize.argtypes = [p, p, p, p, u32, p]
-            L.seqcdc_range_finalize.restype = ctypes.c_int
+        L.seqcdc_range_max_cuts.argtypes = [u64, u64, P]
+        L.seqcdc_range_max_cuts.restype = u64
+        L.seqcdc_range_chunk.argtypes = [p, u64, u64, u64, u64, P, p, p, p, sz, p]
+        L.seqcdc_range_chunk.restype = ctypes.c_int
+        L.seqcdc_range_resync.argtypes = [p, u64, u64, u64, u64, P, p, p, p, p, p, p]
+        L.seqcdc_range_resync.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -234,3 +234,39 @@ def chunk_batch(data, offsets, p: SeqParams, stream=None):
     if k == NCUTS_BAD_INPUT - (1 << 64):
         raise SeqCDCError("inconsistent batch offsets")
     return cuts[:k], cut_index
+
+
+# ------------------------------------------------------------------ range calls (multi-GPU building blocks)
+def range_max_cuts(buf_len: int, range_len: int, p: SeqParams) -> int:
+    cp = p.c()
+    return int(lib().seqcdc_range_max_cuts(buf_len, range_len, ctypes.byref(cp)))
+
+
+def range_chunk_into(buf, range_len: int, entry: int, global_offset: int, p: SeqParams, cuts, ncuts,
+                     workspace=None, stream=None) -> None:
+    """Asynchronous seqcdc_range_chunk: the chain from local ``entry`` up to its
+    first cut >= range_len, as global offsets, into ``cuts`` / ``ncuts``."""
+    import torch
+    _require_cuda(buf, "buf")
+    if buf.dtype != torch.uint8:
+        raise SeqCDCError("buf must be uint8")
+    cp = p.c()
+    ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    rc = lib().seqcdc_range_chunk(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len, entry,
+                                  global_offset, ctypes.byref(cp), cuts.data_ptr() if cuts.numel() else None,
+                                  ncuts.data_ptr(), ws_ptr, ws_len, _stream_ptr(stream, buf.device))
+    _check(rc, "seqcdc_range_chunk")
+
+
+def range_resync_into(buf, range_len: int, entry: int, global_offset: int, p: SeqParams, spec, spec_n, cuts,
+                      ncuts, status, stream=None) -> None:
+    """Asynchronous seqcdc_range_resync: the true chain from the true entry,
+    re-using the speculative chain ``spec[:spec_n]`` after the first common cut.
+    ``status`` int64 CUDA [4] = merged, re-walked cuts, merge index, overhang."""
+    _require_cuda(buf, "buf")
+    cp = p.c()
+    rc = lib().seqcdc_range_resync(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len, entry,
+                                   global_offset, ctypes.byref(cp), spec.data_ptr() if spec.numel() else None,
+                                   spec_n.data_ptr(), cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(),
+                                   status.data_ptr(), _stream_ptr(stream, buf.device))
+    _check(rc, "seqcdc_range_resync")

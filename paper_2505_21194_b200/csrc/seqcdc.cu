@@ -66,6 +66,8 @@ struct Work {
     uint32_t capL1, capX1; // single: uniform list capacities
     uint64_t G;
     uint64_t total;
+    uint64_t stop;         // single: the chain ends at its first cut >= stop (= total, or a range end)
+    uint64_t out_add;      // single: added to every cut written to d_cuts (range calls: global offset)
     DevParams p;
     // per stream (batch)
     uint32_t *str_first;   // [ns+1]
@@ -110,7 +112,7 @@ __device__ __forceinline__ Seg get_seg(const Work &w, uint32_t s)
         g.E = w.total;
         g.last = (s + 1 == w.nseg1);
         g.lo = (uint64_t)s * w.G;
-        g.hi = g.last ? g.E : g.lo + w.G;
+        g.hi = g.last ? w.stop : g.lo + w.G;
         g.Lcap = w.capL1;
         g.Loff = (uint64_t)s * w.capL1;
         g.Xcap = g.last ? 0 : w.capX1;
@@ -330,6 +332,10 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
     const uint64_t off = wk.rb - abase;                      // relative position -> offset into `in`
     const uint32_t end_rel = wk.end_rel;
     const uint32_t hi_rel = g.last ? FULL : base + (uint32_t)(g.hi - g.lo);
+    // the chain of the stream's last segment ends at its first cut >= stop
+    // (the stream end, or for range calls the range end: the overhang)
+    const uint64_t stop_abs = w.single ? w.stop : g.E;
+    const uint32_t stop_rel = (uint32_t)(stop_abs - off);
     uint64_t *Ls = w.L + g.Loff;
     ListBuf lb{0, 0};
     uint32_t c = base;
@@ -344,6 +350,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
         }
         lb_push(lb, off + c, Ls, lane);
         if ((lb.n & 31) == 0) publish(w.Lcnt + s, lb.n, false, lane);
+        if (c >= stop_rel) break;
         base = c;
     }
     lb_flush(lb, Ls, lane);
@@ -373,7 +380,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
         }
         const uint64_t cut = off + c;
         lb_push(xb, cut, Xs, lane);
-        if (cut == g.E) {
+        if (cut >= stop_abs) {                 // the stream end / the range's overhang
             tgt = TGT_END;
             break;
         }
@@ -422,18 +429,20 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
 // One warp re-walks a whole stream (only when an extension overflowed), in
 // jobs of <= 1 GiB so relative positions stay 32-bit.
 template <int MODE, int MSPEC>
-__device__ uint32_t fallback_stream(const Work &w, Walker &wk, uint64_t S0, uint64_t E, uint64_t *dst, int lane)
+__device__ uint32_t fallback_stream(const Work &w, Walker &wk, uint64_t S0, uint64_t E, uint64_t stop, uint64_t *dst,
+                                    int lane)
 {
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
     ListBuf lb{0, 0};
     uint64_t pos = S0;                   // offset of the current chunk start
 #pragma unroll 1
-    while (pos < E) {
+    while (pos < stop) {
         uint32_t base = walker_begin(wk, abase + pos, abase + E);
         const uint64_t off = wk.rb - abase;
         const uint32_t stop_at = base + JOB_SPAN;
+        const uint32_t stop_rel = (uint32_t)(stop - off < (uint64_t)FULL ? stop - off : FULL);
 #pragma unroll 1
-        while (base < wk.end_rel && base < stop_at) {
+        while (base < wk.end_rel && base < stop_at && base < stop_rel) {
             const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
             lb_push(lb, off + c, dst, lane);
             base = c;
@@ -517,7 +526,8 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
                 walker_init(wk, sm);
                 const uint64_t S0 = w.single ? 0 : w.offs[j], E = w.single ? w.total : w.offs[j + 1];
                 const uint64_t o0 = w.single ? 0 : w.offs[0];
-                const uint32_t n = fallback_stream<MODE, MSPEC>(w, wk, S0, E, w.FB + (S0 - o0) / w.p.mn + j, lane);
+                const uint32_t n = fallback_stream<MODE, MSPEC>(w, wk, S0, E, w.single ? w.stop : E,
+                                                                w.FB + (S0 - o0) / w.p.mn + j, lane);
                 if (lane == 0) {
                     w.seg_count[f] = n;
                     w.entry[f] = ENTRY_DEAD;
@@ -585,15 +595,15 @@ __global__ void __launch_bounds__(256) k_copy(Work w)
             if (s != g.first) continue;
             const uint64_t o0 = w.single ? 0 : w.offs[0];
             const uint64_t *src = w.FB + (g.S0 - o0) / w.p.mn + g.j;
-            for (uint64_t i = lane; i < cnt; i += 32) out[i] = src[i];
+            for (uint64_t i = lane; i < cnt; i += 32) out[i] = src[i] + w.out_add;
             continue;
         }
         if (e == ENTRY_DEAD) continue;
         const uint64_t nl = lc - (uint64_t)(e + 1);
         const uint64_t *Ls = w.L + g.Loff + (e + 1);
-        for (uint64_t i = lane; i < nl; i += 32) out[i] = __ldcg(Ls + i);
+        for (uint64_t i = lane; i < nl; i += 32) out[i] = __ldcg(Ls + i) + w.out_add;
         const uint64_t *Xs = w.X + g.Xoff;
-        for (uint64_t i = lane; i < nx; i += 32) out[nl + i] = __ldcg(Xs + i);
+        for (uint64_t i = lane; i < nx; i += 32) out[nl + i] = __ldcg(Xs + i) + w.out_add;
     }
 }
 
@@ -665,7 +675,7 @@ static int device_info(int &sms, int &occ)
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int sms, int occ, Plan &pl,
-                      bool single)
+                      bool single, uint64_t stop)
 {
     const uint64_t walkers = (uint64_t)sms * occ;
     const uint64_t mx = p->max_size, mn = p->min_size;
@@ -677,7 +687,7 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     G = (G + mx - 1) / mx * mx;
     pl.G = G;
     if (single) {
-        pl.nseg1 = (uint32_t)(total <= G ? 1 : (total + G - 1) / G);
+        pl.nseg1 = (uint32_t)(stop <= G ? 1 : (stop + G - 1) / G);
         pl.nseg_max = pl.nseg1;
         pl.capL1 = (uint32_t)(G / mn + 2);
         pl.capX1 = (uint32_t)(std::min<uint64_t>(K_EXT * G, total) / mn + 2);
@@ -767,9 +777,10 @@ static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, 
     k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
 }
 
-static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total,
-               const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index, uint64_t *d_ncuts,
-               uint8_t *ws, size_t ws_bytes, const Plan &pl, int sms, cudaStream_t st, bool single)
+static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total, uint64_t stop,
+               uint64_t out_add, const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index,
+               uint64_t *d_ncuts, uint8_t *ws, size_t ws_bytes, const Plan &pl, int sms, cudaStream_t st,
+               bool single)
 {
     if (ws_bytes < pl.bytes) return SEQCDC_ENOMEM;
     if (total / pl.G + 2 > STITCH_MAX_SEGS) return SEQCDC_EINVAL;  // one stream's segments fit the stitch smem
@@ -784,6 +795,8 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.capX1 = pl.capX1;
     w.G = pl.G;
     w.total = total;
+    w.stop = stop;
+    w.out_add = out_add;
     w.p.L = p->seq_length;
     w.p.T = p->skip_trigger;
     w.p.S = p->skip_size;
@@ -851,15 +864,15 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
 // single-stream calls keep their [0, n] offsets and cut index in front of the workspace
 constexpr size_t SINGLE_EXTRA = 256;
 
-static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total,
-                   const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index, uint64_t *d_ncuts,
-                   void *d_ws, size_t ws_bytes, cudaStream_t st, bool single_api)
+static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total, uint64_t stop,
+                   uint64_t out_add, const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index,
+                   uint64_t *d_ncuts, void *d_ws, size_t ws_bytes, cudaStream_t st, bool single_api)
 {
     int sms, occ;
     int rc = device_info(sms, occ);
     if (rc) return rc;
     Plan pl;
-    make_plan(total, ns, p, sms, occ, pl, single_api);
+    make_plan(total, ns, p, sms, occ, pl, single_api, stop);
     const size_t extra = single_api ? SINGLE_EXTRA : 0;
     uint8_t *ws = (uint8_t *)d_ws;
     bool owned = false;
@@ -877,8 +890,8 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
         d_cut_index = offs + 2;
         k_single_offsets<<<1, 1, 0, st>>>(offs, total);
     }
-    rc = run(d_in, d_offsets, ns, total, p, d_cuts, d_cut_index, d_ncuts, ws + extra, pl.bytes, pl, sms, st,
-             single_api);
+    rc = run(d_in, d_offsets, ns, total, stop, out_add, p, d_cuts, d_cut_index, d_ncuts, ws + extra, pl.bytes, pl,
+             sms, st, single_api);
     if (owned) cudaFreeAsync(ws, st);
     return rc;
 }
@@ -940,8 +953,8 @@ SEQCDC_API size_t seqcdc_workspace_size(uint64_t total, uint32_t ns, const seqcd
     }
     Plan pl;
     Plan pb;
-    make_plan(total, ns ? ns : 1, p, sms, occ, pl, ns <= 1);
-    make_plan(total, ns ? ns : 1, p, sms, occ, pb, false);
+    make_plan(total, ns ? ns : 1, p, sms, occ, pl, ns <= 1, total);
+    make_plan(total, ns ? ns : 1, p, sms, occ, pb, false, total);
     return std::max(pl.bytes, pb.bytes) + SINGLE_EXTRA;
 }
 
@@ -957,7 +970,8 @@ SEQCDC_API int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets
         k_empty<<<1, 1, 0, st>>>(d_cut_index, d_ncuts);
         return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
     }
-    return enqueue(d_in, d_offsets, ns, total, p, d_cuts, d_cut_index, d_ncuts, d_ws, ws_bytes, st, false);
+    return enqueue(d_in, d_offsets, ns, total, total, 0, p, d_cuts, d_cut_index, d_ncuts, d_ws, ws_bytes, st,
+                   false);
 }
 
 SEQCDC_API int seqcdc_chunk(const uint8_t *d_in, uint64_t n, const seqcdc_params_t *p, uint64_t *d_cuts,
@@ -966,7 +980,31 @@ SEQCDC_API int seqcdc_chunk(const uint8_t *d_in, uint64_t n, const seqcdc_params
     if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
     if (!d_ncuts) return SEQCDC_EINVAL;
     if (n && (!d_in || !d_cuts)) return SEQCDC_EINVAL;
-    return enqueue(d_in, nullptr, 1, n, p, d_cuts, nullptr, d_ncuts, d_ws, ws_bytes, (cudaStream_t)stream, true);
+    return enqueue(d_in, nullptr, 1, n, n, 0, p, d_cuts, nullptr, d_ncuts, d_ws, ws_bytes, (cudaStream_t)stream,
+                   true);
+}
+
+SEQCDC_API uint64_t seqcdc_range_max_cuts(uint64_t buf_len, uint64_t range_len, const seqcdc_params_t *p)
+{
+    if (!p || !p->min_size) return 0;
+    const uint64_t span = std::min<uint64_t>(buf_len, range_len + p->max_size);
+    return span / p->min_size + 2;
+}
+
+SEQCDC_API int seqcdc_range_chunk(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                                  uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
+                                  uint64_t *d_ncuts, void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
+    if (!d_ncuts || range_len > buf_len || entry > range_len) return SEQCDC_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (entry >= range_len) {     // no chunk starts inside the range
+        if (cudaMemsetAsync(d_ncuts, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
+        return SEQCDC_OK;
+    }
+    if (!d_buf || !d_cuts) return SEQCDC_EINVAL;
+    return enqueue(d_buf + entry, nullptr, 1, buf_len - entry, range_len - entry, global_offset + entry, p, d_cuts,
+                   nullptr, d_ncuts, d_ws, ws_bytes, st, true);
 }
 
 SEQCDC_API int seqcdc_profile_enable(int on)

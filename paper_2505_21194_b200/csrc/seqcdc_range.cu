@@ -1,0 +1,194 @@
+// seqcdc_range.cu -- the seam re-synchronisation step of the multi-GPU layer
+// (include/seqcdc.h "Range calls").
+//
+// A stream sharded over P ranks is chunked by every rank speculatively from its
+// range start (seqcdc_range_chunk, in seqcdc.cu).  Rank r's true first chunk
+// starts at the overhang of rank r-1 (its first cut >= R_r), which is only
+// known after an exchange.  seqcdc_range_resync re-walks rank r's chain from
+// that true entry until it reaches a cut that is also in the speculative list:
+// "the next cut depends only on the previous cut" (f(base)
+// reads only [base, f(base)) and the stream end), so from a common cut on both
+// chains are identical and the speculative suffix is reused as is.
+//
+// One warp walks (latency-bound; typically tens of chunks, SURVEY.md [MC-3]);
+// a grid-stride kernel then appends the reused suffix.  No host sync.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/seqcdc.h"
+#include "seqcdc_device.cuh"
+
+#define SEQCDC_API extern "C" __attribute__((visibility("default")))
+
+namespace seqcdc {
+namespace {
+
+enum { ST_MERGED = 0, ST_M = 1, ST_J = 2, ST_OVERHANG = 3 };
+
+struct ResyncArgs {
+    const uint8_t *buf;
+    uint64_t buf_len, stop, entry, gofs;
+    const uint64_t *spec;     // speculative cut list (global offsets, ascending)
+    const uint64_t *spec_n;   // its length (device)
+    uint64_t *out, *ncuts, *status;
+    DevParams p;
+};
+
+struct Spec {                 // a 32-entry window of the speculative list, one entry per lane
+    uint64_t j, k;            // index of window entry 0; list length
+    uint32_t nv;
+    uint64_t v;
+};
+
+__device__ __forceinline__ void spec_load(const ResyncArgs &a, Spec &s, int lane)
+{
+    s.nv = (uint32_t)(s.k - s.j < 32 ? s.k - s.j : 32);
+    s.v = lane < (int)s.nv ? __ldcg(a.spec + s.j + lane) : 0;
+}
+
+// index of `cut` in the speculative list, or -1 (cuts are queried in ascending order)
+__device__ __forceinline__ int64_t spec_find(const ResyncArgs &a, Spec &s, uint64_t cut, int lane)
+{
+#pragma unroll 1
+    while (s.nv) {
+        const uint64_t last = __shfl_sync(FULL, s.v, s.nv - 1);
+        if (last < cut) {
+            s.j += s.nv;
+            spec_load(a, s, lane);
+            continue;
+        }
+        const uint32_t hit = __ballot_sync(FULL, lane < (int)s.nv && s.v == cut);
+        return hit ? (int64_t)(s.j + __ffs(hit) - 1) : -1;
+    }
+    return -1;
+}
+
+template <int MODE, int MSPEC>
+__global__ void __launch_bounds__(32) k_resync(ResyncArgs a)
+{
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x;
+    Walker wk;
+    walker_init(wk, smem);
+    const uint64_t abase = (uint64_t)(uintptr_t)a.buf;
+    Spec sp{0, *a.spec_n, 0, 0};
+    spec_load(a, sp, lane);
+    uint64_t vbuf = 0;            // 32 output cuts buffered in lanes
+    uint32_t m = 0;
+    int64_t j = -1;
+    uint64_t pos = a.entry, last = a.entry;
+#pragma unroll 1
+    while (pos < a.stop && j < 0) {
+        uint32_t base = walker_begin(wk, abase + pos, abase + a.buf_len);
+        const uint64_t off = wk.rb - abase;
+        const uint32_t stop_at = base + JOB_SPAN;
+#pragma unroll 1
+        while (base < wk.end_rel && base < stop_at) {
+            const uint32_t c = resolve<MODE, MSPEC>(wk, a.p, base, lane);
+            last = off + c;
+            const uint64_t g = a.gofs + last;
+            if (lane == (int)(m & 31)) vbuf = g;
+            m++;
+            if ((m & 31) == 0) a.out[m - 32 + lane] = vbuf;
+            j = spec_find(a, sp, g, lane);
+            base = c;
+            if (j >= 0 || last >= a.stop) break;
+        }
+        pos = off + base;
+        if (last >= a.stop) break;
+    }
+    walker_finish(wk);
+    const uint32_t r = m & 31;
+    if (lane < (int)r) a.out[m - r + lane] = vbuf;
+    if (lane == 0) {
+        a.status[ST_MERGED] = j >= 0 ? 1 : 0;
+        a.status[ST_M] = m;
+        a.status[ST_J] = (uint64_t)j;
+        a.status[ST_OVERHANG] = a.gofs + last;
+    }
+}
+
+// Append the reused speculative suffix spec[j+1 .. k) after the m re-walked cuts.
+__global__ void __launch_bounds__(256) k_resync_tail(ResyncArgs a)
+{
+    const uint64_t merged = a.status[ST_MERGED], m = a.status[ST_M];
+    const uint64_t k = *a.spec_n;
+    const uint64_t j = a.status[ST_J];
+    const uint64_t ns = merged ? k - (j + 1) : 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += stride)
+        a.out[m + i] = __ldcg(a.spec + j + 1 + i);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *a.ncuts = m + ns;
+        if (merged) a.status[ST_OVERHANG] = k ? __ldcg(a.spec + k - 1) : a.status[ST_OVERHANG];
+    }
+}
+
+__global__ void k_resync_empty(uint64_t *ncuts, uint64_t *status, uint64_t overhang)
+{
+    *ncuts = 0;
+    status[ST_MERGED] = 1;
+    status[ST_M] = 0;
+    status[ST_J] = 0;
+    status[ST_OVERHANG] = overhang;
+}
+
+template <int MODE, int MSPEC>
+void launch(const ResyncArgs &a, cudaStream_t st)
+{
+    static_assert(SMEM_WALK <= 48 * 1024, "the resync walker fits the default smem limit");
+    k_resync<MODE, MSPEC><<<1, 32, SMEM_WALK, st>>>(a);
+    k_resync_tail<<<148, 256, 0, st>>>(a);
+}
+
+}  // namespace
+}  // namespace seqcdc
+
+using namespace seqcdc;
+
+SEQCDC_API int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                                   uint64_t global_offset, const seqcdc_params_t *p, const uint64_t *d_spec,
+                                   const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
+                                   uint64_t *d_status, void *stream)
+{
+    if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
+    if (!d_ncuts || !d_status || !d_spec_n || range_len > buf_len || entry > range_len) return SEQCDC_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (entry >= range_len) {
+        k_resync_empty<<<1, 1, 0, st>>>(d_ncuts, d_status, global_offset + entry);
+        return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
+    }
+    if (!d_buf || !d_cuts || !d_spec) return SEQCDC_EINVAL;
+    ResyncArgs a;
+    memset(&a, 0, sizeof(a));
+    a.buf = d_buf;
+    a.buf_len = buf_len;
+    a.stop = range_len;
+    a.entry = entry;
+    a.gofs = global_offset;
+    a.spec = d_spec;
+    a.spec_n = d_spec_n;
+    a.out = d_cuts;
+    a.ncuts = d_ncuts;
+    a.status = d_status;
+    a.p.L = p->seq_length;
+    a.p.T = p->skip_trigger;
+    a.p.S = p->skip_size;
+    a.p.M = p->seq_length - 1;
+    a.p.mn = (uint32_t)p->min_size;
+    a.p.mx = (uint32_t)p->max_size;
+    a.p.mnL = (uint32_t)p->min_size - p->seq_length;
+    const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
+    if (p->mode == SEQCDC_INCREASING) {
+        if (ms == 4) launch<0, 4>(a, st);
+        else if (ms == 0) launch<0, 0>(a, st);
+        else launch<0, -1>(a, st);
+    } else {
+        if (ms == 4) launch<1, 4>(a, st);
+        else if (ms == 0) launch<1, 0>(a, st);
+        else launch<1, -1>(a, st);
+    }
+    return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
+}

@@ -1,0 +1,174 @@
+"""Multi-GPU SeqCDC: one huge stream sharded into contiguous ranges, one rank per GPU
+(BASELINE config 5).
+
+Why it shards: "the next cut depends only on the previous cut" -- f(base)
+reads only [base, f(base)) and the stream end (P:179 sub-minimum skip, P:189
+content skip, P:266 max cut all restart from the chunk start).  So every rank
+chunks its own range at once, speculatively, as if a chunk started at its range
+start; only the seam needs fixing, and the fix is local once the previous
+rank's overhang (its first cut >= this range's start) is known.
+
+Protocol, per rank r of P (SPMD; ``torch.distributed``, NCCL on GPUs, gloo in
+the CPU tests):
+
+1. ``spec``: the chain from the range start R_r, up to its first cut >= R_{r+1}
+   (the overhang O_r).  Rank 0's chain is the true one (the stream starts there).
+2. all_gather (O_r, count_r).
+3. Rank r > 0 re-synchronises from the true entry O_{r-1}: re-walk until a cut
+   coincides with the speculative chain (then the rest is reused).  If the
+   re-walk reaches R_{r+1} without merging (phase-locked data), rank r's
+   overhang changes.
+4. all_gather (O_r, count_r).  If every overhang equals the one its successor
+   used, the result is final; otherwise the ranks whose entry changed repeat
+   3-4 (at most P-1 rounds; normally one).
+5. Exclusive prefix of the counts = each rank's first global cut index.
+
+The cut lists stay sharded: rank r owns the chunks that START in [R_r, R_{r+1}),
+i.e. cuts (O_{r-1}, O_r] -- concatenated over ranks they are exactly the
+single-stream cut list.
+
+The byte work is done by a backend; ``CudaRangeBackend`` drives the C-ABI range
+calls (seqcdc_range_chunk / seqcdc_range_resync) and is the only product
+backend.  The CPU tests plug in an oracle-based backend to check the protocol
+itself with world_size > 1 over gloo.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Any
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class Shard:
+    """Rank-local piece of a stream: ``buf`` = bytes [global_offset,
+    global_offset + len(buf)): the range (first ``range_len`` bytes) plus a
+    right halo of >= max_size - 1 bytes, or, for the last rank, exactly the
+    rest of the stream."""
+
+    buf: Any
+    range_len: int
+    global_offset: int
+
+
+@dataclass
+class Chain:
+    """A backend's cut list for one shard: ``count`` cuts (global offsets)
+    ending at ``overhang`` (the first cut >= the range end, or the stream end)."""
+
+    cuts: Any
+    count: int
+    overhang: int
+    extra: dict = field(default_factory=dict)
+
+
+@dataclass
+class ShardResult:
+    cuts: Any            # this rank's true cuts (global offsets): cuts[:count]
+    count: int
+    first_index: int     # global index of cuts[0] in the whole stream's list
+    total: int           # number of cuts of the whole stream
+    rounds: int          # exchange rounds after the speculative pass (1 normally)
+    resync_cuts: int     # cuts re-walked by this rank
+    entry: int           # global offset where this rank's first chunk starts
+
+
+def _allgather_i64(values, group, device):
+    t = torch.tensor(values, dtype=torch.int64, device=device)
+    ws = dist.get_world_size(group)
+    out = [torch.empty_like(t) for _ in range(ws)]
+    dist.all_gather(out, t, group=group)
+    return torch.stack(out).cpu().tolist()
+
+
+def chunk_sharded(shard: Shard, backend, group=None, comm_device=None) -> ShardResult:
+    """Run the sharded protocol for this rank (collective: every rank calls it)."""
+    P = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    dev = comm_device if comm_device is not None else backend.comm_device
+    if P > 1 and r < P - 1 and shard.range_len < backend.max_size:
+        raise ValueError("a non-final range must hold at least max_size bytes")
+    spec = backend.spec(shard)
+    info = _allgather_i64([spec.overhang, spec.count], group, dev)
+    cur, cur_entry = spec, shard.global_offset
+    rounds, rewalked = 0, 0
+    while True:
+        true_entry = info[r - 1][0] if r > 0 else shard.global_offset
+        changed = 0
+        if true_entry != cur_entry:
+            cur = backend.resync(shard, true_entry - shard.global_offset, spec)
+            rewalked = cur.extra.get("rewalked", 0)
+            cur_entry, changed = true_entry, 1
+        new = _allgather_i64([cur.overhang, cur.count, changed], group, dev)
+        rounds += 1
+        stable = all(new[k][0] == info[k][0] for k in range(P))
+        info = new
+        if stable:
+            break
+        if rounds > P + 1:
+            raise RuntimeError("seam re-synchronisation did not converge")
+    counts = [row[1] for row in info]
+    return ShardResult(cur.cuts, cur.count, sum(counts[:r]), sum(counts), rounds, rewalked, cur_entry)
+
+
+class CudaRangeBackend:
+    """The product backend: the C-ABI range calls on the rank's GPU.  Buffers
+    are allocated once per shard size and reused across calls."""
+
+    def __init__(self, params, device=None, stream=None):
+        from . import SeqParams  # noqa: F401  (type of params)
+        self.p = params
+        self.max_size = params.max_size
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.comm_device = self.device
+        self.stream = stream
+        self._key = None
+
+    def _alloc(self, shard: Shard):
+        from . import range_max_cuts, workspace_size
+        key = (shard.buf.numel(), shard.range_len)
+        if key == self._key:
+            return
+        n, rl = key
+        cap = max(range_max_cuts(n, rl, self.p), 1)
+        dev = self.device
+        self.spec_cuts = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.out_cuts = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.spec_n = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.out_n = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.ws = torch.empty(workspace_size(n, 1, self.p), dtype=torch.uint8, device=dev)
+        self.host = torch.empty(8, dtype=torch.int64, pin_memory=True)
+        self._key = key
+
+    def _read(self, cuts, ncuts, extra=None) -> list[int]:
+        # one small D2H: count, last cut (the overhang) and the status words
+        k = ncuts.clone()
+        parts = [k, cuts[(k - 1).clamp_min(0)]] + ([extra] if extra is not None else [])
+        with torch.cuda.stream(self.stream) if self.stream is not None else torch.cuda.device(self.device):
+            v = torch.cat(parts)
+            self.host[: v.numel()].copy_(v, non_blocking=True)
+        (self.stream or torch.cuda.current_stream(self.device)).synchronize()
+        return [int(x) for x in self.host[: v.numel()].tolist()]
+
+    def spec(self, shard: Shard) -> Chain:
+        from . import range_chunk_into
+        self._alloc(shard)
+        range_chunk_into(shard.buf, shard.range_len, 0, shard.global_offset, self.p, self.spec_cuts, self.spec_n,
+                         workspace=self.ws, stream=self.stream)
+        k, last = self._read(self.spec_cuts, self.spec_n)
+        if k == 0:
+            last = shard.global_offset
+        return Chain(self.spec_cuts, k, last)
+
+    def resync(self, shard: Shard, entry: int, spec: Chain) -> Chain:
+        from . import range_resync_into
+        self._alloc(shard)
+        range_resync_into(shard.buf, shard.range_len, entry, shard.global_offset, self.p, spec.cuts, self.spec_n,
+                          self.out_cuts, self.out_n, self.status, stream=self.stream)
+        k, last, *st = self._read(self.out_cuts, self.out_n, self.status)
+        if k == 0:
+            last = shard.global_offset + entry
+        return Chain(self.out_cuts, k, last, {"merged": bool(st[0]), "rewalked": int(st[1])})

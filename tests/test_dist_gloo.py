@@ -1,0 +1,102 @@
+"""The multi-GPU sharding protocol (paper_2505_21194_b200/dist.py) over real
+torch.distributed process groups on the CPU (gloo, world_size 2..4), with the
+oracle-based range backend: the concatenated per-rank cut lists must equal the
+single-stream oracle cut list exactly, including on phase-locked data where
+the seam re-synchronisation needs several exchange rounds."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+
+CASES = {
+    # name: (bytes builder, params, range lengths as fractions or explicit)
+    "uniform8k": (lambda: synth.fill_host("uniform", 21, 0, 3 << 20), oracle.table1(8)),
+    "markov4k_dec": (lambda: synth.fill_host("markov", 22, 0, 2 << 20), oracle.table1(4, 1)),
+    "rampmix8k": (lambda: synth.fill_host("rampmix", 23, 0, 2 << 20), oracle.table1(8)),
+    # phase-locked: constant data -> cuts at k*max; a range start that is not a
+    # multiple of max never merges, so overhang changes cascade over ranks
+    "zeros": (lambda: np.zeros((1 << 20) + 12345, np.uint8), oracle.table1(8)),
+    # strictly decreasing bytes in Increasing mode: forced cuts + skips everywhere
+    "dec_ramp": (lambda: ((255 - np.arange((1 << 20) + 777)) % 256).astype(np.uint8), oracle.Params(0, 5, 3, 40, 4096, 16384)),
+}
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _bounds(n, P, max_size, uneven):
+    if uneven:
+        w = np.arange(1, P + 1, dtype=np.float64)
+        cuts = np.floor(np.cumsum(w) / w.sum() * n).astype(np.int64)
+    else:
+        cuts = np.array([(n * (k + 1)) // P for k in range(P)], dtype=np.int64)
+    b = [0] + cuts.tolist()
+    b[-1] = n
+    for k in range(1, P):               # every non-final range holds >= max bytes
+        b[k] = max(b[k], b[k - 1] + max_size)
+    assert b[P - 1] < n
+    return b
+
+
+def _worker(rank, P, port, case, uneven, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        from paper_2505_21194_b200.dist import Shard, chunk_sharded
+        from tests.oracle_range import OracleRangeBackend
+        build, p = CASES[case]
+        b = build()
+        n = b.size
+        R = _bounds(n, P, p.max_size, uneven)
+        lo, hi = R[rank], R[rank + 1]
+        end = n if rank == P - 1 else min(n, hi + p.max_size)
+        shard = Shard(b[lo:end], hi - lo, lo)
+        res = chunk_sharded(shard, OracleRangeBackend(p))
+        cuts = [int(c) for c in np.asarray(res.cuts)[: res.count]]
+        allc = [None] * P
+        dist.all_gather_object(allc, (rank, res.first_index, res.total, res.rounds, cuts))
+        if rank == 0:
+            q.put(allc)
+    finally:
+        dist.destroy_process_group()
+
+
+RUNS = [(2, c) for c in CASES] + [(3, "markov4k_dec"), (3, "zeros"), (3, "dec_ramp"), (4, "uniform8k"), (4, "zeros")]
+
+
+@pytest.mark.parametrize("P,case", RUNS)
+def test_sharded_equals_single_stream(P, case):
+    if case in ("zeros", "dec_ramp") and P == 3:
+        uneven = True
+    else:
+        uneven = P == 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, P, port, case, uneven, q)) for r in range(P)]
+    for pr in procs:
+        pr.start()
+    allc = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    build, p = CASES[case]
+    want = oracle.chunk(build(), p)
+    got = []
+    for rank, first, total, rounds, cuts in sorted(allc):
+        assert first == len(got), (rank, first, len(got))
+        got += cuts
+        assert total == want.size
+    assert np.array_equal(np.asarray(got, np.uint64), want), case
+    if case == "zeros" and P >= 3:
+        assert max(r[3] for r in allc) >= 2      # overhang changes cascaded (several rounds)

@@ -1,0 +1,145 @@
+"""GPU parity of the multi-GPU building blocks (seqcdc_range_chunk /
+seqcdc_range_resync) and of the sharded protocol driving them.  One GPU:
+ranks are emulated as separate processes on cuda:0 exchanging over gloo --
+their kernels never wait on one another, so this is safe on one device."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2505_21194_b200 as sc  # noqa: E402
+
+
+def _sp(p):
+    return sc.SeqParams(p.mode, p.seq_length, p.skip_trigger, p.skip_size, p.min_size, p.max_size)
+
+
+def _oracle_chain(buf, start, range_len, gofs, p):
+    cuts, base = [], start
+    while base < range_len:
+        c = oracle.next_cut(buf, base, p)
+        cuts.append(gofs + c)
+        base = c
+    return np.asarray(cuts, np.uint64)
+
+
+CASES = [("uniform", 31, oracle.table1(8)), ("markov", 32, oracle.table1(4, 1)), ("rampmix", 33, oracle.table1(8)),
+         ("zeroheavy", 34, oracle.table1(16))]
+
+
+@pytest.mark.parametrize("kind,seed,p", CASES)
+@pytest.mark.parametrize("G", [0, 1 << 16])
+def test_range_chunk_and_resync(kind, seed, p, G):
+    sc.set_segment_bytes(G)
+    try:
+        n = 6 << 20
+        b = synth.fill_host(kind, seed, 0, n)
+        sp = _sp(p)
+        for lo, hi in [(0, 2 << 20), (1234567, 3 << 20), (5 << 20, n), (777, 777 + p.max_size)]:
+            end = n if hi == n else min(n, hi + p.max_size)
+            buf_h = b[lo:end]
+            buf = torch.from_numpy(buf_h).cuda()
+            cap = sc.range_max_cuts(buf.numel(), hi - lo, sp)
+            spec = torch.empty(cap, dtype=torch.int64, device="cuda")
+            spec_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+            sc.range_chunk_into(buf, hi - lo, 0, lo, sp, spec, spec_n)
+            got = spec[: int(spec_n.item())].cpu().numpy().astype(np.uint64)
+            assert np.array_equal(got, _oracle_chain(buf_h, 0, hi - lo, lo, p)), (kind, lo, hi)
+            # the true chain from the true entry: the oracle's first cut >= lo
+            full = oracle.chunk(b, p)
+            starts = np.concatenate([[0], full]).astype(np.uint64)
+            entry = int(starts[starts >= lo][0])      # first chunk start >= lo
+            out = torch.empty(cap, dtype=torch.int64, device="cuda")
+            out_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+            status = torch.zeros(4, dtype=torch.int64, device="cuda")
+            sc.range_resync_into(buf, hi - lo, entry - lo, lo, sp, spec, spec_n, out, out_n, status)
+            got = out[: int(out_n.item())].cpu().numpy().astype(np.uint64)
+            want = full[(full > entry) & (full <= (full[full >= hi][0] if hi < n else n))]
+            assert np.array_equal(got, want), (kind, lo, hi, got[:4], want[:4])
+            st = status.cpu().tolist()
+            assert st[3] == int(want[-1])
+            # resync from a non-cut entry equals the chain from there
+            sc.range_resync_into(buf, hi - lo, 1, lo, sp, spec, spec_n, out, out_n, status)
+            got = out[: int(out_n.item())].cpu().numpy().astype(np.uint64)
+            assert np.array_equal(got, _oracle_chain(buf_h, 1, hi - lo, lo, p))
+    finally:
+        sc.set_segment_bytes(0)
+
+
+def test_range_entry_at_end_and_errors():
+    p = _sp(oracle.table1(8))
+    buf = torch.zeros(100, dtype=torch.uint8, device="cuda")
+    cuts = torch.empty(8, dtype=torch.int64, device="cuda")
+    nc = torch.full((1,), 7, dtype=torch.int64, device="cuda")
+    sc.range_chunk_into(buf, 100, 100, 5, p, cuts, nc)
+    assert int(nc.item()) == 0
+    with pytest.raises(sc.SeqCDCError):
+        sc.range_chunk_into(buf, 100, 101, 5, p, cuts, nc)
+    with pytest.raises(sc.SeqCDCError):
+        sc.range_chunk_into(buf, 50, 51, 0, p, cuts, nc)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, P, port, kind, seed, n, pidx, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        from paper_2505_21194_b200.dist import CudaRangeBackend, Shard, chunk_sharded
+        p = _sp(SHARD_PARAMS[pidx])
+        lo, hi = n * rank // P, n * (rank + 1) // P
+        end = n if rank == P - 1 else min(n, hi + p.max_size)
+        buf = torch.empty(end - lo, dtype=torch.uint8, device="cuda")
+        if kind == "zeros":
+            buf.zero_()
+        else:
+            synth.fill_device(kind, seed, lo, buf)
+        be = CudaRangeBackend(p)
+        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=torch.device("cpu"))
+        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=torch.device("cpu"))   # buffers reused
+        cuts = res.cuts[: res.count].cpu().numpy().tolist()
+        allc = [None] * P
+        dist.all_gather_object(allc, (rank, res.first_index, res.total, res.rounds, cuts))
+        if rank == 0:
+            q.put(allc)
+    finally:
+        dist.destroy_process_group()
+
+
+SHARD_PARAMS = [oracle.table1(8), oracle.table1(4, 1), oracle.table1(16)]
+
+
+@pytest.mark.parametrize("P,kind,seed,n,pidx", [(2, "rampmix", 41, 24 << 20, 0), (3, "markov", 42, 20 << 20, 1),
+                                                 (4, "uniform", 43, 30 << 20, 2), (3, "zeros", 0, 5 << 20, 0)])
+def test_sharded_protocol_on_one_gpu(P, kind, seed, n, pidx):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, P, port, kind, seed, n, pidx, q)) for r in range(P)]
+    for pr in procs:
+        pr.start()
+    allc = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    b = np.zeros(n, np.uint8) if kind == "zeros" else synth.fill_host(kind, seed, 0, n)
+    want = oracle.chunk(b, SHARD_PARAMS[pidx])
+    got = []
+    for rank, first, total, rounds, cuts in sorted(allc):
+        assert first == len(got)
+        got += cuts
+        assert total == want.size
+    assert np.array_equal(np.asarray(got, np.uint64), want)
