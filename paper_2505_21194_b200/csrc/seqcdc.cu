@@ -49,12 +49,12 @@ constexpr uint64_t CNT_MASK = DONE_BIT - 1;
 constexpr int32_t TGT_END = -2;
 constexpr int32_t TGT_OVERFLOW = -3;
 constexpr int64_t ENTRY_DEAD = -2;
-constexpr uint32_t K_EXT = 4;             // extension budget, in segments
+constexpr uint32_t K_EXT = 8;             // extension budget, in segments
 constexpr uint64_t G_FLOOR_CHUNKS = 32;   // minimum segment length, in max_size units
 constexpr uint64_t G_CEIL = 64ull << 20;  // keeps a chain's span (G + K_EXT*G + max) far below REL_CLAMP
 constexpr uint32_t STITCH_MAX_SEGS = 8000;
 
-enum { C_NSEG = 0, C_NEXT = 1, C_NFLAG = 2, C_BAD = 3, C_NWORDS = 8 };
+enum { C_NSEG = 0, C_NEXT = 1, C_BAD = 3, C_DONE = 4, C_OVF = 5, C_NWORDS = 8 };
 
 struct Work {
     // inputs
@@ -71,7 +71,6 @@ struct Work {
     DevParams p;
     // per stream (batch)
     uint32_t *str_first;   // [ns+1]
-    uint32_t *str_flag;    // [ns]
     // per segment (batch)
     uint64_t *seg_lo, *seg_hi;
     uint32_t *seg_stream;
@@ -84,6 +83,7 @@ struct Work {
     int64_t *midx;
     int64_t *entry;
     uint64_t *seg_count, *seg_out;
+    uint32_t *cont_cnt;    // cuts of the continuation walk appended after X_s (stitch)
     // lists
     uint64_t *L, *X, *FB;
     uint32_t *ctrl;
@@ -206,7 +206,6 @@ __global__ void __launch_bounds__(1024) k_setup(Work w)
         w.str_first[w.ns] = (uint32_t)nseg;
         w.ctrl[C_NSEG] = (uint32_t)nseg;
         w.ctrl[C_NEXT] = 0;
-        w.ctrl[C_NFLAG] = 0;
         w.ctrl[C_BAD] = 0;
     }
     __syncthreads();
@@ -258,9 +257,10 @@ __device__ __forceinline__ void lb_flush(ListBuf &b, uint64_t *dst, int lane)
 }
 
 // Publish the first n entries of a spec list (release), optionally final.
+// The entries were written by all lanes; the warp barrier orders them before
+// lane 0's (cumulative) release store of the count.
 __device__ __forceinline__ void publish(uint64_t *cntp, uint32_t n, bool done, int lane)
 {
-    __threadfence();
     __syncwarp();
     if (lane == 0) st_release_u64(cntp, (uint64_t)n | (done ? DONE_BIT : 0));
 }
@@ -335,7 +335,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
     // the chain of the stream's last segment ends at its first cut >= stop
     // (the stream end, or for range calls the range end: the overhang)
     const uint64_t stop_abs = w.single ? w.stop : g.E;
-    const uint32_t stop_rel = (uint32_t)(stop_abs - off);
+    const uint32_t stop_rel = stop_abs - off < (uint64_t)FULL ? (uint32_t)(stop_abs - off) : FULL;
     uint64_t *Ls = w.L + g.Loff;
     ListBuf lb{0, 0};
     uint32_t c = base;
@@ -360,6 +360,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
             w.Xcnt[s] = 0;
             w.target[s] = TGT_END;
             w.midx[s] = -1;
+            w.cont_cnt[s] = 0;
         }
         return;
     }
@@ -403,6 +404,106 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
         w.Xcnt[s] = xb.n;
         w.target[s] = tgt;
         w.midx[s] = mi;
+        w.cont_cnt[s] = 0;
+        if (tgt == TGT_OVERFLOW) atomicOr(w.ctrl + C_OVF, 1u);
+    }
+}
+
+// ------------------------------------------------------------------ 2. stitch (+continuation, +scan for one stream)
+// FB slot of the continuation of segment s that starts at offset `from`: on the
+// valid path continuations cover disjoint, increasing position ranges, and a
+// chain covering [a, b] has at most (b-a)/min + 1 cuts, so `from/min + s` never
+// overlaps the next one.
+__device__ __forceinline__ uint64_t *cont_slot(const Work &w, uint32_t s, uint64_t from)
+{
+    return w.FB + (from - (w.single ? 0 : w.offs[0])) / w.p.mn + s;
+}
+
+// Continue the valid chain of segment s past its exhausted extension budget:
+// walk from `from` (its last extension cut, a true cut) until a cut coincides
+// with the chain owning its region (all lists are complete now) or the stream
+// (range) ends.  One warp; positions re-based every JOB_SPAN bytes.
+template <int MODE, int MSPEC>
+__device__ uint32_t continue_chain(const Work &w, Walker &wk, const Seg &g, uint32_t s, uint64_t from,
+                                   int32_t &tgt, int64_t &mi, int lane)
+{
+    const uint64_t abase = (uint64_t)(uintptr_t)w.in;
+    const uint64_t stop = w.single ? w.stop : g.E;
+    uint64_t *dst = cont_slot(w, s, from);
+    ListBuf lb{0, 0};
+    Cursor cur{-1, 0, 0, 0};
+    uint64_t t_lo = 0, t_Loff = 0;
+    tgt = TGT_END;
+    mi = -1;
+    uint64_t pos = from;
+    bool done = false;
+#pragma unroll 1
+    while (!done && pos < stop) {
+        uint32_t base = walker_begin(wk, abase + pos, abase + g.E);
+        const uint64_t off = wk.rb - abase;
+        const uint32_t stop_at = base + JOB_SPAN;
+#pragma unroll 1
+        while (base < wk.end_rel && base < stop_at) {
+            const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+            const uint64_t cut = off + c;
+            lb_push(lb, cut, dst, lane);
+            base = c;
+            if (cut >= stop) {
+                done = true;
+                break;
+            }
+            const uint32_t t = g.first + (uint32_t)((cut - g.S0) / w.G);
+            if ((int64_t)t != cur.t) {
+                t_lo = seg_start(w, g, t);
+                t_Loff = w.single ? (uint64_t)t * w.capL1 : w.Loff[t];
+            }
+            int64_t idx;
+            if (check_cut(w, cur, t, t_lo, t_Loff, cut, idx, lane) == CK_MERGE) {
+                tgt = (int32_t)t;
+                mi = idx;
+                done = true;
+                break;
+            }
+        }
+        pos = off + base;
+    }
+    lb_flush(lb, dst, lane);
+    return lb.n;
+}
+
+// Single stream: follow merges from the stream start (32 segments per step)
+// and continue every valid extension that exhausted its budget; the result
+// is written back as that segment's target / merge index.  One warp.
+template <int MODE, int MSPEC>
+__device__ void fix_overflows(const Work &w, Walker &wk, int lane)
+{
+    const uint32_t k = w.nseg1;
+    uint32_t cur = 0;
+#pragma unroll 1
+    while (cur + 1 < k) {
+        const uint32_t i = cur + lane;
+        const int32_t t = i + 1 < k ? __ldcg(w.target + i) : 0;
+        const uint32_t nb = __ballot_sync(FULL, i + 1 < k && t != (int32_t)(i + 1));
+        if (!nb) {
+            cur += 32;
+            continue;
+        }
+        const uint32_t ic = cur + __ffs(nb) - 1;
+        int32_t tj = __ldcg(w.target + ic);
+        if (tj == TGT_OVERFLOW) {
+            const Seg g = get_seg(w, ic);
+            const uint64_t from = __ldcg(w.X + g.Xoff + __ldcg(w.Xcnt + ic) - 1);
+            int64_t mj;
+            const uint32_t n = continue_chain<MODE, MSPEC>(w, wk, g, ic, from, tj, mj, lane);
+            if (lane == 0) {
+                w.cont_cnt[ic] = n;
+                w.target[ic] = tj;
+                w.midx[ic] = mj;
+            }
+            __syncwarp();
+        }
+        if (tj < 0) break;                 // the stream (range) ends on this path
+        cur = (uint32_t)tj;
     }
 }
 
@@ -412,7 +513,7 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x;
     Walker wk;
-    walker_init(wk, smem);
+    walker_init(wk, smem, w.p, lane);
     const uint32_t nseg = w.ctrl[C_BAD] ? 0u : nseg_total(w);
 #pragma unroll 1
     for (;;) {
@@ -422,49 +523,36 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
         if (s >= nseg) break;
         walk_segment<MODE, MSPEC>(w, wk, s, lane);
     }
-    walker_finish(wk);
-}
-
-// ------------------------------------------------------------------ 2. stitch (+fallback, +scan for one stream)
-// One warp re-walks a whole stream (only when an extension overflowed), in
-// jobs of <= 1 GiB so relative positions stay 32-bit.
-template <int MODE, int MSPEC>
-__device__ uint32_t fallback_stream(const Work &w, Walker &wk, uint64_t S0, uint64_t E, uint64_t stop, uint64_t *dst,
-                                    int lane)
-{
-    const uint64_t abase = (uint64_t)(uintptr_t)w.in;
-    ListBuf lb{0, 0};
-    uint64_t pos = S0;                   // offset of the current chunk start
-#pragma unroll 1
-    while (pos < stop) {
-        uint32_t base = walker_begin(wk, abase + pos, abase + E);
-        const uint64_t off = wk.rb - abase;
-        const uint32_t stop_at = base + JOB_SPAN;
-        const uint32_t stop_rel = (uint32_t)(stop - off < (uint64_t)FULL ? stop - off : FULL);
-#pragma unroll 1
-        while (base < wk.end_rel && base < stop_at && base < stop_rel) {
-            const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
-            lb_push(lb, off + c, dst, lane);
-            base = c;
+    if (w.single) {
+        // the last walker to finish continues any extension on the valid path
+        // that ran out of budget (rare: phase-locked data), so k_post only
+        // has to follow merges
+        __syncwarp();
+        uint32_t last = 0;
+        if (lane == 0) {
+            __threadfence();
+            last = atomicAdd(w.ctrl + C_DONE, 1u) == gridDim.x - 1;
         }
-        pos = off + base;
+        if (__shfl_sync(FULL, last, 0)) {
+            __threadfence();
+            if (*(volatile uint32_t *)(w.ctrl + C_OVF)) fix_overflows<MODE, MSPEC>(w, wk, lane);
+        }
     }
-    lb_flush(lb, dst, lane);
     walker_finish(wk);
-    return lb.n;
 }
 
+// ------------------------------------------------------------------ 2. stitch (batches)
 template <int MODE, int MSPEC>
 __global__ void __launch_bounds__(1024) k_stitch(Work w)
 {
     extern __shared__ __align__(128) uint8_t sm[];
-    __shared__ uint32_t flag;
     if (w.ctrl[C_BAD]) return;
-    // layout: [ring | barriers | tg[K] | mi[K] | en[K]]
-    int32_t *tg = (int32_t *)(sm + SMEM_WALK);
+    // layout: [ring + barriers | tg[K] | mi[K] | en[K]]
+    const uint32_t ring = walker_smem(w.p);
+    int32_t *tg = (int32_t *)(sm + ring);
     const uint32_t kmax = STITCH_MAX_SEGS;
-    int64_t *mi = (int64_t *)(sm + SMEM_WALK + 4 * kmax);
-    int64_t *en = (int64_t *)(sm + SMEM_WALK + 12 * kmax);
+    int64_t *mi = (int64_t *)(sm + ring + 4 * kmax);
+    int64_t *en = (int64_t *)(sm + ring + 12 * kmax);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (uint32_t j = blockIdx.x; j < w.ns; j += gridDim.x) {
         const uint32_t f = w.single ? 0 : w.str_first[j];
@@ -473,7 +561,7 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
             if (threadIdx.x == 0) {
                 w.entry[f] = -1;
                 w.seg_count[f] = w.Lcnt[f] & CNT_MASK;
-                if (!w.single) w.str_flag[j] = 0;
+                w.cont_cnt[f] = 0;
             }
             continue;
         }
@@ -482,10 +570,13 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
             tg[i] = t >= 0 ? t - (int32_t)f : t;
             mi[i] = w.midx[f + i];
             en[i] = ENTRY_DEAD;
+            w.cont_cnt[f + i] = 0;
         }
-        if (threadIdx.x == 0) flag = 0;
         __syncthreads();
         if (wid == 0) {
+            // follow merges from the stream start (the only chain right from its start)
+            Walker wk;
+            walker_init(wk, sm, w.p, lane);
             uint32_t cur = 0;
             int64_t ent = -1;
 #pragma unroll 1
@@ -503,47 +594,31 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
                 }
                 const uint32_t ic = cur + js;
                 if (ic + 1 == k) break;               // the stream's last segment ends at E
-                const int32_t tj = tg[ic];
-                if (tj == TGT_END) break;
-                if (tj < 0) {                         // overflow (or never set)
-                    if (lane == 0) flag = 1;
-                    break;
+                int32_t tj = tg[ic];
+                int64_t mj = mi[ic];
+                if (tj == TGT_OVERFLOW) {             // extension budget exhausted: continue it here
+                    const Seg g = get_seg(w, f + ic);
+                    const uint32_t nx = w.Xcnt[f + ic];
+                    const uint64_t from = __ldcg(w.X + g.Xoff + nx - 1);
+                    int32_t t2;
+                    const uint32_t n = continue_chain<MODE, MSPEC>(w, wk, g, f + ic, from, t2, mj, lane);
+                    if (lane == 0) w.cont_cnt[f + ic] = n;
+                    tj = t2 >= 0 ? t2 - (int32_t)f : t2;
                 }
-                ent = mi[ic];
+                if (tj < 0) break;                    // reached the end of the stream / range
+                ent = mj;
                 cur = (uint32_t)tj;
             }
+            walker_finish(wk);
         }
         __syncthreads();
-        if (flag) {
-            // pathological stream: one warp re-walks it end to end into FB
-            for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
-                w.seg_count[f + i] = 0;
-                w.entry[f + i] = ENTRY_DEAD;
-            }
-            __syncthreads();
-            if (wid == 0) {
-                Walker wk;
-                walker_init(wk, sm);
-                const uint64_t S0 = w.single ? 0 : w.offs[j], E = w.single ? w.total : w.offs[j + 1];
-                const uint64_t o0 = w.single ? 0 : w.offs[0];
-                const uint32_t n = fallback_stream<MODE, MSPEC>(w, wk, S0, E, w.single ? w.stop : E,
-                                                                w.FB + (S0 - o0) / w.p.mn + j, lane);
-                if (lane == 0) {
-                    w.seg_count[f] = n;
-                    w.entry[f] = ENTRY_DEAD;
-                }
-            }
-            if (threadIdx.x == 0 && !w.single) w.str_flag[j] = 1;
-            if (threadIdx.x == 0 && w.single) w.ctrl[C_NFLAG] = 1;
-        } else {
-            for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
-                const int64_t e = en[i];
-                uint64_t c = 0;
-                if (e != ENTRY_DEAD) c = (w.Lcnt[f + i] & CNT_MASK) - (uint64_t)(e + 1) + w.Xcnt[f + i];
-                w.seg_count[f + i] = c;
-                w.entry[f + i] = e;
-            }
-            if (threadIdx.x == 0 && !w.single) w.str_flag[j] = 0;
+        for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) {
+            const int64_t e = en[i];
+            uint64_t c = 0;
+            if (e != ENTRY_DEAD)
+                c = (w.Lcnt[f + i] & CNT_MASK) - (uint64_t)(e + 1) + w.Xcnt[f + i] + w.cont_cnt[f + i];
+            w.seg_count[f + i] = c;
+            w.entry[f + i] = e;
         }
         __syncthreads();
     }
@@ -589,21 +664,141 @@ __global__ void __launch_bounds__(256) k_copy(Work w)
         const int64_t e = w.entry[s];
         const uint64_t lc = w.Lcnt[s] & CNT_MASK, nx = w.Xcnt[s], o = w.seg_out[s], cnt = w.seg_count[s];
         uint64_t *out = w.cuts + o;
-        const Seg g = get_seg(w, s);
-        const bool flagged = w.single ? (w.ctrl[C_NFLAG] != 0) : (w.str_flag[g.j] != 0);
-        if (flagged) {
-            if (s != g.first) continue;
-            const uint64_t o0 = w.single ? 0 : w.offs[0];
-            const uint64_t *src = w.FB + (g.S0 - o0) / w.p.mn + g.j;
-            for (uint64_t i = lane; i < cnt; i += 32) out[i] = src[i] + w.out_add;
-            continue;
-        }
         if (e == ENTRY_DEAD) continue;
+        const Seg g = get_seg(w, s);
         const uint64_t nl = lc - (uint64_t)(e + 1);
         const uint64_t *Ls = w.L + g.Loff + (e + 1);
         for (uint64_t i = lane; i < nl; i += 32) out[i] = __ldcg(Ls + i) + w.out_add;
         const uint64_t *Xs = w.X + g.Xoff;
         for (uint64_t i = lane; i < nx; i += 32) out[nl + i] = __ldcg(Xs + i) + w.out_add;
+        const uint64_t nc = cnt - nl - nx;   // continuation (stitch) cuts
+        if (nc) {
+            const uint64_t *Cs = cont_slot(w, s, __ldcg(Xs + nx - 1));
+            for (uint64_t i = lane; i < nc; i += 32) out[nl + nx + i] = __ldcg(Cs + i) + w.out_add;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ single stream: stitch + scan + copy in one launch
+// Every CTA follows the merges from the stream start and scans the per-segment
+// valid counts itself (a few KB of L2 reads each: no grid-wide barrier), then
+// copies its share of the segments' valid cuts to d_cuts.
+__device__ void smem_scan_excl(uint64_t *a, uint32_t n)
+{
+    __shared__ uint64_t wsum[32];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nt = blockDim.x;
+    const uint32_t per = (n + nt - 1) / nt;
+    const uint32_t b0 = tid * per, b1 = min(n, b0 + per);
+    uint64_t loc = 0;
+    for (uint32_t i = b0; i < b1; i++) loc += a[i];
+    uint64_t inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(FULL, inc, o);
+        if ((int)lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const uint64_t x = lane < nt / 32 ? wsum[lane] : 0;
+        uint64_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(FULL, xi, o);
+            if ((int)lane >= o) xi += t;
+        }
+        wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    uint64_t run = wsum[wid] + inc - loc;
+    for (uint32_t i = b0; i < b1; i++) {
+        const uint64_t v = a[i];
+        a[i] = run;
+        run += v;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) k_post(Work w)
+{
+    extern __shared__ __align__(128) uint8_t sm[];
+    const uint32_t k = w.nseg1;
+    int32_t *tg = (int32_t *)sm;                          // [K]
+    int64_t *en = (int64_t *)(sm + 4 * STITCH_MAX_SEGS);  // [K] entry index (-1: from the start)
+    uint64_t *cnt = (uint64_t *)(sm + 12 * STITCH_MAX_SEGS);  // [K] merge index, then count, then offset
+    const uint32_t tid = threadIdx.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    int ok = 1;
+    for (uint32_t i = tid; i < k; i += blockDim.x) {
+        const int32_t t = __ldcg(w.target + i);
+        tg[i] = t;
+        cnt[i] = (uint64_t)__ldcg(w.midx + i);
+        en[i] = ENTRY_DEAD;
+        if (i + 1 < k && t != (int32_t)(i + 1)) ok = 0;
+    }
+    ok = __syncthreads_and(ok);
+    if (ok) {                                   // every extension merged into its successor
+        for (uint32_t i = tid; i < k; i += blockDim.x) en[i] = i ? (int64_t)cnt[i - 1] : -1;
+    } else if (wid == 0) {                      // follow the merges (some chain skipped a segment)
+        uint32_t cur = 0;
+        int64_t ent = -1;
+#pragma unroll 1
+        for (;;) {
+            const uint32_t i = cur + lane;
+            const int32_t t = i < k ? tg[i] : 0;
+            const bool pass = (i + 1 < k) && t == (int32_t)(i + 1);
+            const uint32_t nb = __ballot_sync(FULL, !pass);
+            const int js = nb ? __ffs(nb) - 1 : 32;
+            if (lane <= js && i < k) en[i] = lane == 0 ? ent : (int64_t)cnt[i - 1];
+            if (js == 32) {
+                ent = (int64_t)cnt[cur + 31];
+                cur += 32;
+                continue;
+            }
+            const uint32_t ic = cur + js;
+            if (ic + 1 == k) break;
+            const int32_t tj = tg[ic];
+            if (tj < 0) break;                  // end of stream / range (overflows were fixed in k_walk)
+            ent = (int64_t)cnt[ic];
+            cur = (uint32_t)tj;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < k; i += blockDim.x) {
+        const int64_t e = en[i];
+        cnt[i] = e == ENTRY_DEAD ? 0
+                                 : (__ldcg(w.Lcnt + i) & CNT_MASK) - (uint64_t)(e + 1) + __ldcg(w.Xcnt + i) +
+                                       __ldcg(w.cont_cnt + i);
+    }
+    __syncthreads();
+    const uint64_t last = cnt[k - 1];
+    smem_scan_excl(cnt, k);
+    if (blockIdx.x == 0 && tid == 0) {
+        const uint64_t total = cnt[k - 1] + last;
+        w.cut_index[0] = 0;
+        w.cut_index[1] = total;
+        *w.ncuts = total;
+    }
+    // copy: one warp per segment
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t s2 = blockIdx.x * (blockDim.x >> 5) + wid; s2 < k; s2 += nw) {
+        const int64_t e = en[s2];
+        if (e == ENTRY_DEAD) continue;
+        const Seg g = get_seg(w, s2);
+        uint64_t *out = w.cuts + cnt[s2];
+        const uint64_t lc = __ldcg(w.Lcnt + s2) & CNT_MASK, nx = __ldcg(w.Xcnt + s2), nc = __ldcg(w.cont_cnt + s2);
+        const uint64_t nl = lc - (uint64_t)(e + 1);
+        const uint64_t *Ls = w.L + g.Loff + (e + 1);
+        const uint64_t add = w.out_add;
+#pragma unroll 4
+        for (uint64_t i = lane; i < nl; i += 32) out[i] = __ldcg(Ls + i) + add;
+        const uint64_t *Xs = w.X + g.Xoff;
+#pragma unroll 2
+        for (uint64_t i = lane; i < nx; i += 32) out[nl + i] = __ldcg(Xs + i) + add;
+        if (nc) {
+            const uint64_t *Cs = cont_slot(w, s2, __ldcg(Xs + nx - 1));
+            for (uint64_t i = lane; i < nc; i += 32) out[nl + nx + i] = __ldcg(Cs + i) + add;
+        }
     }
 }
 
@@ -613,37 +808,58 @@ __global__ void k_empty(uint64_t *cut_index, uint64_t *ncuts)
     *ncuts = 0;
 }
 
-__global__ void k_single_offsets(uint64_t *offs, uint64_t n)
-{
-    offs[0] = 0;
-    offs[1] = n;
-}
 
 // ------------------------------------------------------------------ host side
 struct Plan {
     uint64_t G, nseg_max, L_items, X_items, FB_items;
     uint32_t nseg1, capL1, capX1;
     size_t bytes;
-    size_t o_ctrl, o_Lcnt, o_str_first, o_str_flag, o_seg_lo, o_seg_hi, o_seg_stream, o_Loff, o_Xoff,
+    size_t o_ctrl, o_Lcnt, o_str_first, o_cont_cnt, o_seg_lo, o_seg_hi, o_seg_stream, o_Loff, o_Xoff,
         o_Lcap, o_Xcap, o_Xcnt, o_target, o_midx, o_entry, o_seg_count, o_seg_out, o_L, o_X, o_FB;
     uint32_t walk_grid;
 };
 
-static int g_sms = 0, g_occ = 0;
+static int g_sms = 0;
 static uint64_t g_force_G = 0;
 static std::mutex g_mu;
 static cudaMemPool_t g_pool[64];
 static bool g_pool_ok[64];
 
+constexpr uint32_t MAX_RING = SMEM_WALK;
+constexpr uint32_t STITCH_SMEM = SMEM_WALK + 20 * STITCH_MAX_SEGS;
+
 template <int MODE, int MSPEC>
 static void set_attrs()
 {
-    cudaFuncSetAttribute((const void *)k_walk<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_WALK);
+    cudaFuncSetAttribute((const void *)k_walk<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_WALK);
     cudaFuncSetAttribute((const void *)k_stitch<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_WALK + 20 * STITCH_MAX_SEGS);
+                         STITCH_SMEM);
+    cudaFuncSetAttribute((const void *)k_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 20 * STITCH_MAX_SEGS);
 }
 
-static int device_info(int &sms, int &occ)
+static int env_int(const char *name, int dflt)
+{
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+// Ring geometry for a parameter set: the prefetch must reach past the
+// sub-minimum region plus about two examined windows, so that a chunk
+// step does not wait a full HBM round trip.  Blocks grow with min_size so the
+// slot count stays <= 8.
+static void ring_geometry(const seqcdc_params_t *, DevParams &d)
+{
+    d.bs = BLK_SHIFT;
+    d.nb = NBLK;
+    d.ah = AHEAD;
+}
+
+static int g_occ_by_smem[MAX_RING / 1024 + 2];
+static DevParams g_last_geo;
+static int g_last_occ;
+
+static int device_info(int &sms, int &occ, uint32_t smem = SMEM_WALK)
 {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_sms) {
@@ -657,18 +873,19 @@ static int device_info(int &sms, int &occ)
         set_attrs<1, 4>();
         set_attrs<1, 0>();
         set_attrs<1, -1>();
-        int occ_ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4>, 32, SMEM_WALK) != cudaSuccess)
-            return SEQCDC_ECUDA;
-        if (const char *e = getenv("SEQCDC_WALKERS_PER_SM")) {
-            int v = atoi(e);
-            if (v > 0 && v < occ_) occ_ = v;
-        }
-        g_occ = occ_ > 0 ? occ_ : 1;
         g_sms = nsm;
     }
+    const uint32_t key = std::min<uint32_t>(smem / 1024, MAX_RING / 1024 + 1);
+    if (!g_occ_by_smem[key]) {
+        int occ_ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4>, 32, smem) != cudaSuccess)
+            return SEQCDC_ECUDA;
+        const int v = env_int("SEQCDC_WALKERS_PER_SM", 0);
+        if (v > 0 && v < occ_) occ_ = v;
+        g_occ_by_smem[key] = occ_ > 0 ? occ_ : 1;
+    }
     sms = g_sms;
-    occ = g_occ;
+    occ = g_occ_by_smem[key];
     return SEQCDC_OK;
 }
 
@@ -699,7 +916,7 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
         pl.L_items = total / mn + 2 * pl.nseg_max + 2;
         pl.X_items = K_EXT * (total / mn) + 2 * pl.nseg_max + 2;
     }
-    pl.FB_items = total / mn + ns + 2;
+    pl.FB_items = total / mn + ns + pl.nseg_max + 2;
     pl.walk_grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(pl.nseg_max, walkers));
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -712,7 +929,7 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     pl.o_Lcnt = o;  // contiguous with ctrl: one memset resets both
     o = align_up(o + 8 * S, 256);
     pl.o_str_first = take(4ull * (ns + 1));
-    pl.o_str_flag = take(4ull * ns);
+    pl.o_cont_cnt = take(4 * S);
     pl.o_seg_lo = take(single ? 0 : 8 * S);
     pl.o_seg_hi = take(single ? 0 : 8 * S);
     pl.o_seg_stream = take(single ? 0 : 4 * S);
@@ -769,16 +986,21 @@ template <int MODE, int MSPEC>
 static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
 {
     prof_mark(pr, 1, st);
-    k_walk<MODE, MSPEC><<<pl.walk_grid, 32, SMEM_WALK, st>>>(w);
+    k_walk<MODE, MSPEC><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
     prof_mark(pr, 2, st);
-    const uint32_t sgrid = w.single ? 1u : (uint32_t)std::min<uint64_t>(w.ns, 2ull * sms);
-    k_stitch<MODE, MSPEC><<<sgrid, 1024, SMEM_WALK + 20 * STITCH_MAX_SEGS, st>>>(w);
-    if (!w.single) k_scan<<<1, 1024, 0, st>>>(w);
+    if (w.single) {
+        const uint32_t pgrid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(sms, (w.nseg1 + 31) / 32));
+        k_post<<<pgrid, 1024, 20 * STITCH_MAX_SEGS, st>>>(w);
+        return;
+    }
+    const uint32_t sgrid = (uint32_t)std::min<uint64_t>(w.ns, 2ull * sms);
+    k_stitch<MODE, MSPEC><<<sgrid, 1024, walker_smem(w.p) + 20 * STITCH_MAX_SEGS, st>>>(w);
+    k_scan<<<1, 1024, 0, st>>>(w);
     k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
 }
 
 static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total, uint64_t stop,
-               uint64_t out_add, const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index,
+               uint64_t out_add, const seqcdc_params_t *p, const DevParams &geo, uint64_t *d_cuts, uint64_t *d_cut_index,
                uint64_t *d_ncuts, uint8_t *ws, size_t ws_bytes, const Plan &pl, int sms, cudaStream_t st,
                bool single)
 {
@@ -804,10 +1026,13 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.p.mn = (uint32_t)p->min_size;
     w.p.mx = (uint32_t)p->max_size;
     w.p.mnL = (uint32_t)p->min_size - p->seq_length;
+    w.p.bs = geo.bs;
+    w.p.nb = geo.nb;
+    w.p.ah = geo.ah;
     w.ctrl = (uint32_t *)(ws + pl.o_ctrl);
     w.Lcnt = (uint64_t *)(ws + pl.o_Lcnt);
     w.str_first = (uint32_t *)(ws + pl.o_str_first);
-    w.str_flag = (uint32_t *)(ws + pl.o_str_flag);
+    w.cont_cnt = (uint32_t *)(ws + pl.o_cont_cnt);
     w.seg_lo = (uint64_t *)(ws + pl.o_seg_lo);
     w.seg_hi = (uint64_t *)(ws + pl.o_seg_hi);
     w.seg_stream = (uint32_t *)(ws + pl.o_seg_stream);
@@ -868,9 +1093,13 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
                    uint64_t out_add, const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index,
                    uint64_t *d_ncuts, void *d_ws, size_t ws_bytes, cudaStream_t st, bool single_api)
 {
+    DevParams geo;
+    ring_geometry(p, geo);
     int sms, occ;
-    int rc = device_info(sms, occ);
+    int rc = device_info(sms, occ, walker_smem(geo));
     if (rc) return rc;
+    g_last_geo = geo;
+    g_last_occ = occ;
     Plan pl;
     make_plan(total, ns, p, sms, occ, pl, single_api, stop);
     const size_t extra = single_api ? SINGLE_EXTRA : 0;
@@ -884,14 +1113,13 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
         if (cudaMallocFromPoolAsync((void **)&ws, pl.bytes + extra, pool, st) != cudaSuccess) return SEQCDC_ENOMEM;
         owned = true;
     }
-    if (single_api) {
+    if (single_api) {                      // [0, n] offsets are implicit; the cut index lives in the workspace
         uint64_t *offs = (uint64_t *)ws;
         d_offsets = offs;
         d_cut_index = offs + 2;
-        k_single_offsets<<<1, 1, 0, st>>>(offs, total);
     }
-    rc = run(d_in, d_offsets, ns, total, stop, out_add, p, d_cuts, d_cut_index, d_ncuts, ws + extra, pl.bytes, pl,
-             sms, st, single_api);
+    rc = run(d_in, d_offsets, ns, total, stop, out_add, p, geo, d_cuts, d_cut_index, d_ncuts, ws + extra, pl.bytes,
+             pl, sms, st, single_api);
     if (owned) cudaFreeAsync(ws, st);
     return rc;
 }
@@ -899,6 +1127,16 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
 }  // namespace seqcdc
 
 using namespace seqcdc;
+
+// internal, used by seqcdc_range.cu (hidden visibility: not part of the ABI)
+void seqcdc_ring_geometry(const seqcdc_params_t *p, uint32_t *bs, uint32_t *nb, uint32_t *ah)
+{
+    DevParams d;
+    ring_geometry(p, d);
+    *bs = d.bs;
+    *nb = d.nb;
+    *ah = d.ah;
+}
 
 SEQCDC_API int seqcdc_validate_params(const seqcdc_params_t *p)
 {
@@ -946,8 +1184,10 @@ SEQCDC_API uint64_t seqcdc_max_cuts_batch(uint64_t total, uint32_t ns, const seq
 SEQCDC_API size_t seqcdc_workspace_size(uint64_t total, uint32_t ns, const seqcdc_params_t *p)
 {
     if (seqcdc_validate_params(p)) return 0;
+    DevParams geo;
+    ring_geometry(p, geo);
     int sms, occ;
-    if (device_info(sms, occ)) {
+    if (device_info(sms, occ, walker_smem(geo))) {   // no device: an upper bound (32 CTAs/SM)
         sms = 148;
         occ = 32;
     }
@@ -1061,10 +1301,12 @@ SEQCDC_API const char *seqcdc_strerror(int code)
 
 SEQCDC_API const char *seqcdc_build_info(void)
 {
-    static char buf[192];
+    static char buf[256];
     int sms = 0, occ = 0;
     device_info(sms, occ);
-    snprintf(buf, sizeof(buf), "seqcdc sm_100a blk=%u nblk=%u ahead=%u ring=%u win_pairs=%u k_ext=%u walkers=%dx%d",
-             BLK, NBLK, AHEAD, RING, WIN_PAIRS, K_EXT, sms, occ);
+    const DevParams g = g_last_geo;
+    snprintf(buf, sizeof(buf),
+             "seqcdc sm_100a cp.async ring last call: blk=%u nblk=%u ahead=%u walkers=%dx%d; win_pairs=%u k_ext=%u",
+             1u << g.bs, g.nb, g.ah, sms, g_last_occ, WIN_PAIRS, K_EXT);
     return buf;
 }

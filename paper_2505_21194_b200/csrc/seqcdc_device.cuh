@@ -62,7 +62,11 @@ struct DevParams {
     uint32_t L, T, S, M;   // M = L-1 favourable pairs per run
     uint32_t mn, mx;       // min/max chunk sizes (<= 2^28, validated on the host)
     uint32_t mnL;          // mn - L: offset of the scan anchor from the chunk start
+    uint32_t bs, nb, ah;   // ring geometry (reported; compile-time in this build)
 };
+
+// dynamic shared memory of one walker
+__host__ __device__ __forceinline__ uint32_t walker_smem(const DevParams &) { return SMEM_WALK; }
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -217,7 +221,7 @@ __device__ __forceinline__ void ring_need(Walker &wk, uint32_t need_lo, uint32_t
     wk.b_ok = wk.b_next - AHEAD;
 }
 
-__device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem)
+__device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, const DevParams &, int)
 {
     wk.buf = smem_u32(smem);
     wk.rb = 0;

@@ -22,6 +22,9 @@
 
 #define SEQCDC_API extern "C" __attribute__((visibility("default")))
 
+// internal (seqcdc.cu): the ring geometry every walker of a call uses
+void seqcdc_ring_geometry(const seqcdc_params_t *p, uint32_t *bs, uint32_t *nb, uint32_t *ah);
+
 namespace seqcdc {
 namespace {
 
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(32) k_resync(ResyncArgs a)
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x;
     Walker wk;
-    walker_init(wk, smem);
+    walker_init(wk, smem, a.p, lane);
     const uint64_t abase = (uint64_t)(uintptr_t)a.buf;
     Spec sp{0, *a.spec_n, 0, 0};
     spec_load(a, sp, lane);
@@ -138,8 +141,9 @@ __global__ void k_resync_empty(uint64_t *ncuts, uint64_t *status, uint64_t overh
 template <int MODE, int MSPEC>
 void launch(const ResyncArgs &a, cudaStream_t st)
 {
-    static_assert(SMEM_WALK <= 48 * 1024, "the resync walker fits the default smem limit");
-    k_resync<MODE, MSPEC><<<1, 32, SMEM_WALK, st>>>(a);
+    cudaFuncSetAttribute((const void *)k_resync<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         walker_smem(a.p));
+    k_resync<MODE, MSPEC><<<1, 32, walker_smem(a.p), st>>>(a);
     k_resync_tail<<<148, 256, 0, st>>>(a);
 }
 
@@ -180,6 +184,7 @@ SEQCDC_API int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint6
     a.p.mn = (uint32_t)p->min_size;
     a.p.mx = (uint32_t)p->max_size;
     a.p.mnL = (uint32_t)p->min_size - p->seq_length;
+    seqcdc_ring_geometry(p, &a.p.bs, &a.p.nb, &a.p.ah);
     const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
     if (p->mode == SEQCDC_INCREASING) {
         if (ms == 4) launch<0, 4>(a, st);

@@ -129,7 +129,8 @@ def test_single_stream_kinds(kind, seed, n, p):
 
 @pytest.mark.parametrize("G", [1 << 16, 3 << 16, 1 << 20, 5 << 20])
 @pytest.mark.parametrize("kind,p", [("uniform", oracle.table1(8)), ("markov", oracle.table1(4, 1)),
-                                    ("rampmix", oracle.table1(8)), ("zeroheavy", oracle.table1(16))])
+                                    ("rampmix", oracle.table1(8)), ("zeroheavy", oracle.table1(16)),
+                                    ("uniform", oracle.table1(16))])
 def test_segment_size_independence(G, kind, p):
     """Cut lists do not depend on the speculative segment length (many seams,
     extensions spanning several segments)."""
@@ -203,3 +204,17 @@ def test_config2_full_size():
     for pos in (0, 12345678, n - 70000):
         assert np.array_equal(synth.fill_host("markov", 2, pos, 70000), b[pos:pos + 70000])
     _assert_same(got, oracle.chunk(b, p), "config 2")
+
+
+def test_stream_over_4gib():
+    """A single stream longer than 2^32 bytes (positions re-based inside the
+    walker; the north-star >= 4 GiB case), config-5 data shape, every cut
+    compared with the oracle."""
+    n = (4 << 30) + (3 << 20) + 12345
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    synth.fill_device("rampmix", 5, 0, d)
+    p = oracle.table1(8)
+    got = sc.chunk(d, _sp(p)).cpu().numpy().astype(np.uint64)
+    b = d.cpu().numpy()
+    del d
+    _assert_same(got, oracle.chunk(b, p), "4 GiB+")
