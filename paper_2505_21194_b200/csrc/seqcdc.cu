@@ -238,6 +238,28 @@ __global__ void __launch_bounds__(1024) k_setup(Work w)
 }
 
 // ------------------------------------------------------------------ 1. walk
+// Debug timeline (variant builds with -DSEQCDC_TIMELINE): per segment the
+// globaltimer at walk start, end of the speculative part, end of the extension
+// and the SM id.  Set with seqcdc_debug_timeline().
+#ifdef SEQCDC_TIMELINE
+__device__ uint64_t *g_tl;
+__device__ uint64_t g_tl_cap;
+__device__ __forceinline__ void tl_mark(uint32_t s, int k)
+{
+    if (g_tl && s < g_tl_cap && threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        uint32_t smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_tl[4 * s + k] = t;
+        g_tl[4 * s + 3] = smid;
+    }
+}
+#define TL_MARK(s, k) tl_mark((s), (k))
+#else
+#define TL_MARK(s, k)
+#endif
+
 struct ListBuf {  // 32 cuts buffered in lane registers, written coalesced
     uint64_t v;
     uint32_t n;   // total cuts appended
@@ -326,6 +348,7 @@ __device__ int check_cut(const Work &w, Cursor &c, uint32_t t, uint64_t t_lo, ui
 template <int MODE, int MSPEC>
 __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
 {
+    TL_MARK(s, 0);
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
     const Seg g = get_seg(w, s);
     uint32_t base = walker_begin(wk, abase + g.lo, abase + g.E);
@@ -355,6 +378,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
     }
     lb_flush(lb, Ls, lane);
     publish(w.Lcnt + s, lb.n, true, lane);
+    TL_MARK(s, 1);
     if (!extend) {                       // the stream's last segment: no extension
         if (lane == 0) {
             w.Xcnt[s] = 0;
@@ -400,6 +424,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
         c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
     }
     lb_flush(xb, Xs, lane);
+    TL_MARK(s, 2);
     if (lane == 0) {
         w.Xcnt[s] = xb.n;
         w.target[s] = tgt;
@@ -512,6 +537,7 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
 {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x;
+    asm volatile("griddepcontrol.launch_dependents;");   // let k_post's CTAs queue for the tail
     Walker wk;
     walker_init(wk, smem, w.p, lane);
     const uint32_t nseg = w.ctrl[C_BAD] ? 0u : nseg_total(w);
@@ -722,6 +748,7 @@ __device__ void smem_scan_excl(uint64_t *a, uint32_t n)
 __global__ void __launch_bounds__(1024) k_post(Work w)
 {
     extern __shared__ __align__(128) uint8_t sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // k_walk complete and its writes visible
     const uint32_t k = w.nseg1;
     int32_t *tg = (int32_t *)sm;                          // [K]
     int64_t *en = (int64_t *)(sm + 4 * STITCH_MAX_SEGS);  // [K] entry index (-1: from the start)
@@ -880,6 +907,9 @@ static int device_info(int &sms, int &occ, uint32_t smem = SMEM_WALK)
         int occ_ = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4>, 32, smem) != cudaSuccess)
             return SEQCDC_ECUDA;
+        // 24 walkers per SM measured best (25 -- the smem limit -- leaves almost no L1
+        // and runs ~25% slower on config 2; profiles/r01/sweeps.md)
+        if (occ_ > 24) occ_ = 24;
         const int v = env_int("SEQCDC_WALKERS_PER_SM", 0);
         if (v > 0 && v < occ_) occ_ = v;
         g_occ_by_smem[key] = occ_ > 0 ? occ_ : 1;
@@ -896,9 +926,13 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
 {
     const uint64_t walkers = (uint64_t)sms * occ;
     const uint64_t mx = p->max_size, mn = p->min_size;
+    // segments per walker (x100; tuning knob) and the segment floor in max_size units
+    const uint64_t spw = (uint64_t)std::max(1, env_int("SEQCDC_SEGS_PER_WALKER_X100", 100));
+    const uint64_t floor_chunks = (uint64_t)std::max(1, env_int("SEQCDC_G_FLOOR_CHUNKS", (int)G_FLOOR_CHUNKS));
     uint64_t denom = walkers > 2ull * ns ? walkers - ns : std::max<uint64_t>(walkers / 2, 1);
+    denom = std::max<uint64_t>(1, denom * spw / 100);
     uint64_t G = (total + denom - 1) / denom;
-    G = std::max<uint64_t>(G, G_FLOOR_CHUNKS * mx);
+    G = std::max<uint64_t>(G, floor_chunks * mx);
     if (g_force_G) G = std::max<uint64_t>(g_force_G, mx);
     G = std::min<uint64_t>(G, std::max<uint64_t>(G_CEIL, mx));
     G = (G + mx - 1) / mx * mx;
@@ -989,8 +1023,21 @@ static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, 
     k_walk<MODE, MSPEC><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
     prof_mark(pr, 2, st);
     if (w.single) {
+        // programmatic dependent launch: k_post's CTAs become resident on SMs the
+        // walk's tail leaves idle and wait (griddepcontrol.wait) for its completion
         const uint32_t pgrid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(sms, (w.nseg1 + 31) / 32));
-        k_post<<<pgrid, 1024, 20 * STITCH_MAX_SEGS, st>>>(w);
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3(pgrid);
+        cfg.blockDim = dim3(1024);
+        cfg.dynamicSmemBytes = 20 * STITCH_MAX_SEGS;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pr ? 0 : 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, k_post, w);
         return;
     }
     const uint32_t sgrid = (uint32_t)std::min<uint64_t>(w.ns, 2ull * sms);
@@ -1310,3 +1357,12 @@ SEQCDC_API const char *seqcdc_build_info(void)
              1u << g.bs, g.nb, g.ah, sms, g_last_occ, WIN_PAIRS, K_EXT);
     return buf;
 }
+
+#ifdef SEQCDC_TIMELINE
+SEQCDC_API int seqcdc_debug_timeline(uint64_t *d_buf, uint64_t nseg_cap)
+{
+    if (cudaMemcpyToSymbol(g_tl, &d_buf, sizeof(d_buf)) != cudaSuccess) return SEQCDC_ECUDA;
+    if (cudaMemcpyToSymbol(g_tl_cap, &nseg_cap, sizeof(nseg_cap)) != cudaSuccess) return SEQCDC_ECUDA;
+    return SEQCDC_OK;
+}
+#endif

@@ -43,6 +43,9 @@ namespace seqcdc {
 #ifndef SEQCDC_AHEAD
 #define SEQCDC_AHEAD 4
 #endif
+#ifndef SEQCDC_L2PF
+#define SEQCDC_L2PF 0
+#endif
 constexpr int BLK_SHIFT = SEQCDC_BLK_SHIFT;          // 1 KiB ring blocks
 constexpr uint32_t BLK = 1u << BLK_SHIFT;
 constexpr uint32_t NBLK = SEQCDC_NBLK;               // blocks in the ring (power of two)
@@ -176,6 +179,13 @@ struct Walker {
 __device__ __forceinline__ void ring_issue(Walker &wk, uint32_t b, int lane)
 {
     const uint32_t b0 = b << BLK_SHIFT;
+#if SEQCDC_L2PF > 0
+    {   // pull the block SEQCDC_L2PF blocks further ahead into L2 (one bulk prefetch, no smem)
+        const uint32_t pf = b0 + SEQCDC_L2PF * BLK;
+        if (lane == 0 && pf + BLK <= wk.end_rel)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wk.rb + pf), "r"(BLK) : "memory");
+    }
+#endif
     if (b0 >= wk.lo_rel && b0 + BLK <= wk.end_rel) {
 #pragma unroll
         for (uint32_t k = 0; k < BLK / 512; k++) {

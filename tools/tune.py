@@ -24,15 +24,19 @@ ws = torch.empty(sc.workspace_size(n, 1, p), dtype=torch.uint8, device="cuda")
 for _ in range(3):
     sc.chunk_into(d, p, cuts, nc, workspace=ws)
 torch.cuda.synchronize()
-sc.profile_enable(True)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(steps):
     sc.chunk_into(d, p, cuts, nc, workspace=ws)
 e1.record()
 torch.cuda.synchronize()
-prof, k = sc.profile_collect()
 ms = e0.elapsed_time(e1) / steps
+sc.profile_enable(True)
+for _ in range(steps):
+    sc.chunk_into(d, p, cuts, nc, workspace=ws)
+torch.cuda.synchronize()
+prof, k = sc.profile_collect()
+sc.profile_enable(False)
 print(json.dumps({"kind": kind, "MiB": mib, "avg": avg, "mode": mode, "env": {k2: v for k2, v in os.environ.items()
                   if k2.startswith("SEQCDC")}, "GBps": round(n / ms / 1e6, 1), "ms": round(ms, 4),
                   "walk_ms": round(prof["walk"] / k, 4), "post_ms": round(prof["post"] / k, 4),
