@@ -1351,10 +1351,9 @@ SEQCDC_API const char *seqcdc_build_info(void)
     static char buf[256];
     int sms = 0, occ = 0;
     device_info(sms, occ);
-    const DevParams g = g_last_geo;
     snprintf(buf, sizeof(buf),
-             "seqcdc sm_100a cp.async ring last call: blk=%u nblk=%u ahead=%u walkers=%dx%d; win_pairs=%u k_ext=%u",
-             1u << g.bs, g.nb, g.ah, sms, g_last_occ, WIN_PAIRS, K_EXT);
+             "seqcdc sm_100a cp.async ring blk=%u nblk=%u ahead=%u walkers=%dx%d (last call); win_pairs=%u k_ext=%u",
+             BLK, NBLK, AHEAD, sms, g_last_occ, WIN_PAIRS, K_EXT);
     return buf;
 }
 

@@ -34,23 +34,25 @@
 
 namespace seqcdc {
 
+// Ring geometry (profiles/r01/sweeps.md): 2 KiB blocks (4 x 16-byte cp.async per
+// lane each), 4 slots, 2 blocks (4 KiB) in flight ahead of the window.
 #ifndef SEQCDC_BLK_SHIFT
-#define SEQCDC_BLK_SHIFT 10
+#define SEQCDC_BLK_SHIFT 11
 #endif
 #ifndef SEQCDC_NBLK
-#define SEQCDC_NBLK 8
+#define SEQCDC_NBLK 4
 #endif
 #ifndef SEQCDC_AHEAD
-#define SEQCDC_AHEAD 4
+#define SEQCDC_AHEAD 2
 #endif
 #ifndef SEQCDC_L2PF
 #define SEQCDC_L2PF 0
 #endif
-constexpr int BLK_SHIFT = SEQCDC_BLK_SHIFT;          // 1 KiB ring blocks
+constexpr int BLK_SHIFT = SEQCDC_BLK_SHIFT;          // ring block size (log2)
 constexpr uint32_t BLK = 1u << BLK_SHIFT;
 constexpr uint32_t NBLK = SEQCDC_NBLK;               // blocks in the ring (power of two)
 constexpr uint32_t AHEAD = SEQCDC_AHEAD;             // blocks kept in flight past the window
-constexpr uint32_t RING = BLK * NBLK;                // 8 KiB per walker
+constexpr uint32_t RING = BLK * NBLK;                // 8 KiB per walker (default geometry)
 constexpr uint32_t RING_MASK = RING - 1;
 static_assert(AHEAD + 2 <= NBLK, "ring must hold the window's two blocks plus the lookahead");
 static_assert(BLK >= 512 && BLK % 512 == 0, "a block is whole rounds of 32 x 16-byte copies");

@@ -1,8 +1,9 @@
 cd $GRAFT_REPO_ROOT
-for occ in 18 20 22 23 24 25; do
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 2 1024 4 1 20 >> gpurun_out/sweep9.jsonl 2>&1
-done
-for occ in 20 24 25; do
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 2 4096 4 1 10 >> gpurun_out/sweep9.jsonl 2>&1
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py rampmix 5 4096 8 0 10 >> gpurun_out/sweep9.jsonl 2>&1
+for v in v24 b2n4 b512; do
+  export SEQCDC_LIB=build/v_$v.so
+  python tools/tune.py markov 2 1024 4 1 20 >> gpurun_out/sweep10.jsonl 2>&1
+  SEQCDC_WALKERS_PER_SM=22 python tools/tune.py markov 2 1024 4 1 20 >> gpurun_out/sweep10.jsonl 2>&1
+  SEQCDC_WALKERS_PER_SM=2 python tools/tune.py markov 2 1024 4 1 5 >> gpurun_out/sweep10.jsonl 2>&1
+  python tools/tune.py markov 2 4096 4 1 10 >> gpurun_out/sweep10.jsonl 2>&1
+  SEQCDC_WALKERS_PER_SM=12 python tools/tune.py uniform 1 1024 8 0 >> gpurun_out/sweep10.jsonl 2>&1
 done
