@@ -535,11 +535,11 @@ __device__ void fix_overflows(const Work &w, Walker &wk, int lane)
 template <int MODE, int MSPEC>
 __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
 {
-    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(128) uint8_t ring[RING];
     const int lane = threadIdx.x;
     asm volatile("griddepcontrol.launch_dependents;");   // let k_post's CTAs queue for the tail
     Walker wk;
-    walker_init(wk, smem, w.p, lane);
+    walker_init(wk, ring, w.p, lane);
     const uint32_t nseg = w.ctrl[C_BAD] ? 0u : nseg_total(w);
 #pragma unroll 1
     for (;;) {
@@ -572,13 +572,13 @@ template <int MODE, int MSPEC>
 __global__ void __launch_bounds__(1024) k_stitch(Work w)
 {
     extern __shared__ __align__(128) uint8_t sm[];
+    __shared__ __align__(128) uint8_t ring[RING];
     if (w.ctrl[C_BAD]) return;
-    // layout: [ring + barriers | tg[K] | mi[K] | en[K]]
-    const uint32_t ring = walker_smem(w.p);
-    int32_t *tg = (int32_t *)(sm + ring);
+    // layout: [tg[K] | mi[K] | en[K]]
+    int32_t *tg = (int32_t *)sm;
     const uint32_t kmax = STITCH_MAX_SEGS;
-    int64_t *mi = (int64_t *)(sm + ring + 4 * kmax);
-    int64_t *en = (int64_t *)(sm + ring + 12 * kmax);
+    int64_t *mi = (int64_t *)(sm + 4 * kmax);
+    int64_t *en = (int64_t *)(sm + 12 * kmax);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (uint32_t j = blockIdx.x; j < w.ns; j += gridDim.x) {
         const uint32_t f = w.single ? 0 : w.str_first[j];
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(1024) k_stitch(Work w)
         if (wid == 0) {
             // follow merges from the stream start (the only chain right from its start)
             Walker wk;
-            walker_init(wk, sm, w.p, lane);
+            walker_init(wk, ring, w.p, lane);
             uint32_t cur = 0;
             int64_t ent = -1;
 #pragma unroll 1
@@ -852,14 +852,11 @@ static std::mutex g_mu;
 static cudaMemPool_t g_pool[64];
 static bool g_pool_ok[64];
 
-constexpr uint32_t MAX_RING = SMEM_WALK;
-constexpr uint32_t STITCH_SMEM = SMEM_WALK + 20 * STITCH_MAX_SEGS;
+constexpr uint32_t STITCH_SMEM = 20 * STITCH_MAX_SEGS;
 
 template <int MODE, int MSPEC>
 static void set_attrs()
 {
-    cudaFuncSetAttribute((const void *)k_walk<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_WALK);
     cudaFuncSetAttribute((const void *)k_stitch<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          STITCH_SMEM);
     cudaFuncSetAttribute((const void *)k_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 20 * STITCH_MAX_SEGS);
@@ -882,11 +879,10 @@ static void ring_geometry(const seqcdc_params_t *, DevParams &d)
     d.ah = AHEAD;
 }
 
-static int g_occ_by_smem[MAX_RING / 1024 + 2];
-static DevParams g_last_geo;
+static int g_occ_by_smem[66];
 static int g_last_occ;
 
-static int device_info(int &sms, int &occ, uint32_t smem = SMEM_WALK)
+static int device_info(int &sms, int &occ, uint32_t smem = 0)
 {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_sms) {
@@ -902,7 +898,7 @@ static int device_info(int &sms, int &occ, uint32_t smem = SMEM_WALK)
         set_attrs<1, -1>();
         g_sms = nsm;
     }
-    const uint32_t key = std::min<uint32_t>(smem / 1024, MAX_RING / 1024 + 1);
+    const uint32_t key = std::min<uint32_t>(smem / 1024, 65);
     if (!g_occ_by_smem[key]) {
         int occ_ = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4>, 32, smem) != cudaSuccess)
@@ -1041,7 +1037,7 @@ static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, 
         return;
     }
     const uint32_t sgrid = (uint32_t)std::min<uint64_t>(w.ns, 2ull * sms);
-    k_stitch<MODE, MSPEC><<<sgrid, 1024, walker_smem(w.p) + 20 * STITCH_MAX_SEGS, st>>>(w);
+    k_stitch<MODE, MSPEC><<<sgrid, 1024, STITCH_SMEM, st>>>(w);
     k_scan<<<1, 1024, 0, st>>>(w);
     k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
 }
@@ -1145,7 +1141,6 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
     int sms, occ;
     int rc = device_info(sms, occ, walker_smem(geo));
     if (rc) return rc;
-    g_last_geo = geo;
     g_last_occ = occ;
     Plan pl;
     make_plan(total, ns, p, sms, occ, pl, single_api, stop);

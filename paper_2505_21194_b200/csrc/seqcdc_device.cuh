@@ -70,8 +70,8 @@ struct DevParams {
     uint32_t bs, nb, ah;   // ring geometry (reported; compile-time in this build)
 };
 
-// dynamic shared memory of one walker
-__host__ __device__ __forceinline__ uint32_t walker_smem(const DevParams &) { return SMEM_WALK; }
+// the walker's ring is a static __shared__ array: no dynamic shared memory
+__host__ __device__ __forceinline__ uint32_t walker_smem(const DevParams &) { return 0; }
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -233,9 +233,15 @@ __device__ __forceinline__ void ring_need(Walker &wk, uint32_t need_lo, uint32_t
     wk.b_ok = wk.b_next - AHEAD;
 }
 
+// `ring` is a static __shared__ array of RING bytes in the calling kernel (its
+// shared address is then a link-time constant).
 __device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, const DevParams &, int)
 {
-    wk.buf = smem_u32(smem);
+    // opaque to the compiler: kept in a register instead of being re-derived from
+    // the CTA's shared window id (S2UR, long latency) at every use
+    uint32_t sb = smem_u32(smem);
+    asm volatile("mov.b32 %0, %0;" : "+r"(sb));
+    wk.buf = sb;
     wk.rb = 0;
     wk.lo_rel = wk.end_rel = 0;
     wk.b_next = wk.b_ok = 0;
@@ -297,6 +303,15 @@ __device__ __forceinline__ uint32_t run_mask(uint32_t Fm, uint32_t carry, uint32
 
 // f(base): the cut ending the chunk that starts at relative position `base`
 // (base < end_rel).  Warp-uniform; every lane returns the same value.
+//
+// One round per examined window of 128 pairs (4 per lane).  Both events are
+// located with ballots only (no shuffle-reduction on the critical path):
+//   r = first pair ending a favourable run (ballot + __ffs, "builtin_ffs")
+//   d = the need-th opposing pair: per-lane exclusive prefix of the opposing
+//       counts from three count-bit ballots, the crossing lane by a ballot, the
+//       byte inside it by a SWAR prefix ("pdep + tzcnt").
+// r < d -> cut r+2; d < r -> skip to d+1+S with fresh counters;
+// neither -> next window.  Pairs and bytes come from the warp's ring.
 template <int MODE, int MSPEC>
 __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint32_t base, int lane)
 {
@@ -310,6 +325,7 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
     uint32_t p0 = a & ~3u;
     uint32_t lomask = FULL << (8 * (a & 3u));      // lane 0: pairs below the anchor
     const uint32_t qoff = 4 * (uint32_t)lane;
+    const uint32_t lt_mask = lanemask_lt();
 #pragma unroll 1
     for (;;) {
         {
@@ -323,46 +339,45 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
         const uint32_t y = __funnelshift_r(x, xn, 8);     // y_k = byte q+k+1
         uint32_t lt, gt;
         lt_gt_flags(x, y, lt, gt);
-        uint32_t V = (lane ? FULL : lomask) & H;
-        if (p0 + (WIN_PAIRS - 1) > lim2) {                // window crosses the last pair
-            const int32_t sh = (int32_t)qoff * 8 + 24 - 8 * (int32_t)(lim2 - p0);
-            V &= shr_c(FULL, sh > 0 ? (uint32_t)sh : 0u);
-        }
+        // Pairs past lim2 (the window's tail at the chunk limit) are NOT masked: the
+        // ring bytes there may be stale, so any event found past lim2 is discarded
+        // below (events are taken in pair order, so a stale one can only come after
+        // every valid one).
+        const uint32_t V = (lane ? FULL : lomask) & H;
         const uint32_t Fm = (MODE == 0 ? lt : gt) & V;
         const uint32_t Om = (MODE == 0 ? gt : lt) & V;
         const uint32_t R = run_mask<MSPEC>(Fm, carry, p.M, lane);
-        const uint32_t rmask = __ballot_sync(FULL, R != 0);
         const uint32_t cnt = __popc(Om);
-        const uint32_t total = __reduce_add_sync(FULL, cnt);
-        if (rmask == 0 && total < need) {          // nothing decided in this window
-            need -= total;
+        const uint32_t b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),
+                       b2 = __ballot_sync(FULL, cnt & 4);
+        const uint32_t rmask = __ballot_sync(FULL, R != 0);
+        const uint32_t excl = __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask);
+        const uint32_t dmask = __ballot_sync(FULL, excl + cnt >= need);
+        if ((rmask | dmask) == 0) {                // nothing decided in this window
+            need -= __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
             carry = MSPEC >= 0 ? __shfl_sync(FULL, Fm, 31) : Fm;
             p0 += WIN_PAIRS;
             lomask = FULL;
             if (p0 > lim2) return limit;
             continue;
         }
-        if (rmask) {
-            // first qualifying run in pair order, and the opposing pairs before it
-            const int rl = __ffs(rmask) - 1;
-            const uint32_t rbyte = __shfl_sync(FULL, (uint32_t)(__ffs(R) - 1) >> 3, rl);
-            const uint32_t bm = lane < rl ? FULL : (lane == rl ? (1u << (8 * rbyte)) - 1u : 0u);
-            const uint32_t before = __reduce_add_sync(FULL, __popc(Om & bm));
-            if (before < need) return p0 + 4 * (uint32_t)rl + rbyte + 2;   // boundary after the run
-        }
-        // the need-th opposing pair of this window triggers a skip (it precedes any run)
-        const uint32_t lt_mask = lanemask_lt();
-        const uint32_t b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),
-                       b2 = __ballot_sync(FULL, cnt & 4);
-        const uint32_t excl = __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask);
-        const int dl = __ffs(__ballot_sync(FULL, excl + cnt >= need)) - 1;
-        // in lane dl: the k-th flag (k = need - excl); byte j of pc = flags in bytes 0..j
-        const uint32_t k = need - excl;
+        // per lane: byte of its first run end, byte of its k-th opposing pair
+        // (k = need - excl; byte j of pc = opposing flags in bytes 0..j)
+        const uint32_t rbyte = (uint32_t)(__ffs(R) - 1) >> 3;
         const uint32_t pc = (Om >> 7) * 0x01010101u;
-        const uint32_t ge = ((pc | H) - k * 0x01010101u) & 0x00808080u;
-        const uint32_t d = p0 + 4 * (uint32_t)dl + __shfl_sync(FULL, 3u - __popc(ge), dl);
-        if (p.S >= lim2 - d) return limit;         // skip lands past the last pair (c8)
-        a = d + 1 + p.S;                           // content-defined skip (c3)
+        const uint32_t ge = ((pc | H) - (need - excl) * 0x01010101u) & 0x00808080u;
+        const uint32_t dbyte = 3u - __popc(ge);
+        const uint32_t rl = rmask ? (uint32_t)__ffs(rmask) - 1 : 32u;
+        const uint32_t dl = dmask ? (uint32_t)__ffs(dmask) - 1 : 32u;
+        const uint32_t r = 4 * rl + __shfl_sync(FULL, rbyte, rl & 31);
+        const uint32_t d = 4 * dl + __shfl_sync(FULL, dbyte, dl & 31);
+        if (r < d) {                               // the run completes first: boundary after it
+            const uint32_t ra = p0 + r;
+            return ra <= lim2 ? ra + 2 : limit;
+        }
+        const uint32_t da = p0 + d;                // the need-th opposing pair triggers a skip
+        if (da > lim2 || p.S >= lim2 - da) return limit;   // no skip before the limit / lands past it (c8)
+        a = da + 1 + p.S;                          // content-defined skip (c3)
         need = p.T;
         carry = 0;
         p0 = a & ~3u;

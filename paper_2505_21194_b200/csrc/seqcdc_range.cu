@@ -71,10 +71,10 @@ __device__ __forceinline__ int64_t spec_find(const ResyncArgs &a, Spec &s, uint6
 template <int MODE, int MSPEC>
 __global__ void __launch_bounds__(32) k_resync(ResyncArgs a)
 {
-    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(128) uint8_t ring[RING];
     const int lane = threadIdx.x;
     Walker wk;
-    walker_init(wk, smem, a.p, lane);
+    walker_init(wk, ring, a.p, lane);
     const uint64_t abase = (uint64_t)(uintptr_t)a.buf;
     Spec sp{0, *a.spec_n, 0, 0};
     spec_load(a, sp, lane);
@@ -141,9 +141,7 @@ __global__ void k_resync_empty(uint64_t *ncuts, uint64_t *status, uint64_t overh
 template <int MODE, int MSPEC>
 void launch(const ResyncArgs &a, cudaStream_t st)
 {
-    cudaFuncSetAttribute((const void *)k_resync<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         walker_smem(a.p));
-    k_resync<MODE, MSPEC><<<1, 32, walker_smem(a.p), st>>>(a);
+    k_resync<MODE, MSPEC><<<1, 32, 0, st>>>(a);
     k_resync_tail<<<148, 256, 0, st>>>(a);
 }
 
