@@ -35,6 +35,8 @@ torch.cuda.synchronize()
 L.seqcdc_debug_timeline(None, 0)
 a = tl.cpu().numpy().reshape(-1, 4)
 a = a[a[:, 0] > 0]
+if os.environ.get("TL_SAVE"):
+    np.save(os.environ["TL_SAVE"], a)
 t0 = a[:, 0].min()
 st, sp, ex = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3
 ex = np.where(a[:, 2] > 0, ex, sp)
