@@ -137,3 +137,29 @@ SYNTH_API int synth_batch_layout(uint64_t seed, uint32_t nstreams, uint64_t mean
     }
     return 0;
 }
+
+// ------------------------------------------------------------------ gather (config 4 versions)
+// dst[dst_off .. +len) = (sel ? src1 : src0)[src_off .. +len) for every slice
+// (slices: uint64[n][4] = sel, src_off, dst_off, len; each <= 64 KiB).  Pure
+// byte movement: builds a version of the versioned-backup stream from the
+// previous version and a pool of fresh random bytes.
+__global__ void synth_gather_kernel(uint8_t *dst, const uint8_t *src0, const uint8_t *src1,
+                                    const uint64_t *slices, uint64_t n)
+{
+    for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const uint64_t *s = slices + 4 * i;
+        const uint8_t *src = (s[0] ? src1 : src0) + s[1];
+        uint8_t *d = dst + s[2];
+        const uint64_t len = s[3];
+        for (uint64_t k = threadIdx.x; k < len; k += blockDim.x) d[k] = src[k];
+    }
+}
+
+SYNTH_API int synth_gather_device(uint8_t *dst, const uint8_t *src0, const uint8_t *src1,
+                                  const uint64_t *d_slices, uint64_t n, cudaStream_t stream)
+{
+    if (n == 0) return 0;
+    unsigned grid = (unsigned)(n < 148 * 16 ? n : 148 * 16);
+    synth_gather_kernel<<<grid, 512, 0, stream>>>(dst, src0, src1, d_slices, n);
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
