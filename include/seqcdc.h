@@ -174,6 +174,40 @@ int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_l
                         const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
                         uint64_t *d_status, void *stream);
 
+/*
+ * After chunking (§2): "Each data
+ * chunk is hashed using a collision-resistant hashing algorithm, such as
+ * SHA-256 ... to obtain a fingerprint"; "the fingerprint is compared
+ * against a database of previously observed fingerprints"; space
+ * savings = (original - deduplicated) / original (Eq. 1).
+ * Both calls read the chunk count on the device (d_ncuts, e.g. the one
+ * seqcdc_chunk wrote) so they can be enqueued behind it without a host sync;
+ * max_cuts (host) bounds it and sizes the grids.
+ *
+ * seqcdc_fingerprint: d_digests[32*i .. +32) = SHA-256 (FIPS 180-4) of chunk
+ * i = d_in[c_{i-1} .. c_i), c_{-1} = 0, with c = d_cuts (exclusive ends,
+ * offsets into d_in).  d_digests: device, >= 32*max_cuts bytes, 16-byte
+ * aligned.  Errors: SEQCDC_EINVAL (NULL pointers, misaligned d_digests),
+ * SEQCDC_ECUDA.
+ */
+int seqcdc_fingerprint(const uint8_t *d_in, const uint64_t *d_cuts, const uint64_t *d_ncuts,
+                       uint64_t max_cuts, uint8_t *d_digests, void *stream);
+
+/* Bytes of scratch seqcdc_dedup needs for up to max_cuts chunks (its hash set). */
+size_t seqcdc_dedup_workspace_size(uint64_t max_cuts);
+
+/*
+ * seqcdc_dedup: duplicate detection over the chunks' digests.  Chunk i is a
+ * first occurrence iff no chunk j < i has the same digest; d_first[i] = 1/0
+ * (d_first may be NULL) and *d_unique_bytes = the summed sizes of first
+ * occurrences (the bytes a dedup store keeps).  d_ws/ws_bytes: scratch of
+ * seqcdc_dedup_workspace_size(max_cuts) bytes, or NULL to allocate
+ * stream-ordered.  Deterministic (the smallest index of each digest wins).
+ * Errors: SEQCDC_EINVAL, SEQCDC_ENOMEM, SEQCDC_ECUDA.
+ */
+int seqcdc_dedup(const uint8_t *d_digests, const uint64_t *d_cuts, const uint64_t *d_ncuts, uint64_t max_cuts,
+                 uint8_t *d_first, uint64_t *d_unique_bytes, void *d_workspace, size_t ws_bytes, void *stream);
+
 /* Testing / tuning knob: force the segment length G (rounded up to a
  * multiple of max_size, and to at least max_size) used to split streams into
  * speculative chains; 0 restores the automatic choice.  Process-global.  The

@@ -252,3 +252,43 @@ def chunk_query(data, p: Params) -> np.ndarray:
         cuts.append(cut)
         base = cut
     return np.asarray(cuts, dtype=np.uint64)
+
+
+# --------------------------------------------------------------------------
+# Dedup after chunking (§2): every chunk gets a
+# collision-resistant fingerprint (SHA-256), fingerprints are compared
+# against those already stored, and space savings follow Eq. 1
+# (P:74-76).  Plain definitions: hashlib's SHA-256 and a Python set.
+# --------------------------------------------------------------------------
+def chunk_starts(cuts) -> np.ndarray:
+    cuts = np.asarray(cuts, dtype=np.int64)
+    return np.concatenate([[0], cuts[:-1]]) if cuts.size else np.zeros(0, np.int64)
+
+
+def fingerprints(data, cuts) -> np.ndarray:
+    """SHA-256 digest (32 bytes) of every chunk [c_{i-1}, c_i), c_{-1} = 0."""
+    import hashlib
+    b = _as_u8(data)
+    mv = memoryview(b)
+    cuts = np.asarray(cuts, dtype=np.int64)
+    out = np.empty((cuts.size, 32), dtype=np.uint8)
+    for i, (s, e) in enumerate(zip(chunk_starts(cuts).tolist(), cuts.tolist())):
+        out[i] = np.frombuffer(hashlib.sha256(mv[s:e]).digest(), dtype=np.uint8)
+    return out
+
+
+def dedup(data, cuts):
+    """-> (first_occurrence[k] bool, unique_bytes): chunk i is unique iff no
+    earlier chunk has the same fingerprint; unique bytes = stored
+    bytes; space savings = 1 - unique/total (Eq. 1)."""
+    fp = fingerprints(data, cuts)
+    cuts = np.asarray(cuts, dtype=np.int64)
+    sizes = cuts - chunk_starts(cuts)
+    seen, first, uniq = set(), np.zeros(cuts.size, dtype=bool), 0
+    for i in range(cuts.size):
+        h = fp[i].tobytes()
+        if h not in seen:
+            seen.add(h)
+            first[i] = True
+            uniq += int(sizes[i])
+    return first, uniq

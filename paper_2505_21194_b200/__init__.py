@@ -30,6 +30,7 @@ EXPORTS = (
     "seqcdc_workspace_size", "seqcdc_chunk", "seqcdc_chunk_batch", "seqcdc_strerror",
     "seqcdc_build_info", "seqcdc_set_segment_bytes", "seqcdc_profile_enable", "seqcdc_profile_collect",
     "seqcdc_range_max_cuts", "seqcdc_range_chunk", "seqcdc_range_resync",
+    "seqcdc_fingerprint", "seqcdc_dedup_workspace_size", "seqcdc_dedup",
 )
 
 
@@ -111,6 +112,12 @@ def lib():
         L.seqcdc_range_chunk.restype = ctypes.c_int
         L.seqcdc_range_resync.argtypes = [p, u64, u64, u64, u64, P, p, p, p, p, p, p]
         L.seqcdc_range_resync.restype = ctypes.c_int
+        L.seqcdc_fingerprint.argtypes = [p, p, p, u64, p, p]
+        L.seqcdc_fingerprint.restype = ctypes.c_int
+        L.seqcdc_dedup_workspace_size.argtypes = [u64]
+        L.seqcdc_dedup_workspace_size.restype = sz
+        L.seqcdc_dedup.argtypes = [p, p, p, u64, p, p, p, sz, p]
+        L.seqcdc_dedup.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -270,3 +277,32 @@ def range_resync_into(buf, range_len: int, entry: int, global_offset: int, p: Se
                                    spec_n.data_ptr(), cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(),
                                    status.data_ptr(), _stream_ptr(stream, buf.device))
     _check(rc, "seqcdc_range_resync")
+
+
+# ------------------------------------------------------------------ after chunking: fingerprints + dedup (NEXT-1)
+def fingerprint_into(data, cuts, ncuts, digests, max_cuts=None, stream=None) -> None:
+    """Asynchronous seqcdc_fingerprint: SHA-256 of every chunk into ``digests``
+    (uint8 CUDA [>= 32*max_cuts], 16-byte aligned); the count is read from ``ncuts``."""
+    _require_cuda(data, "data")
+    _require_cuda(digests, "digests")
+    mc = cuts.numel() if max_cuts is None else int(max_cuts)
+    rc = lib().seqcdc_fingerprint(data.data_ptr() if data.numel() else None, cuts.data_ptr() if mc else None,
+                                  ncuts.data_ptr(), mc, digests.data_ptr() if mc else None,
+                                  _stream_ptr(stream, data.device))
+    _check(rc, "seqcdc_fingerprint")
+
+
+def dedup_into(digests, cuts, ncuts, unique_bytes, first=None, max_cuts=None, workspace=None, stream=None) -> None:
+    """Asynchronous seqcdc_dedup: first-occurrence flags (optional uint8 CUDA) and
+    the stored bytes (int64 CUDA [1])."""
+    _require_cuda(digests, "digests")
+    mc = cuts.numel() if max_cuts is None else int(max_cuts)
+    ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    rc = lib().seqcdc_dedup(digests.data_ptr() if mc else None, cuts.data_ptr() if mc else None, ncuts.data_ptr(),
+                            mc, first.data_ptr() if first is not None else None, unique_bytes.data_ptr(), ws_ptr,
+                            ws_len, _stream_ptr(stream, digests.device))
+    _check(rc, "seqcdc_dedup")
+
+
+def dedup_workspace_size(max_cuts: int) -> int:
+    return int(lib().seqcdc_dedup_workspace_size(int(max_cuts)))

@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libseqcdc.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("seqcdc.cu", "seqcdc_device.cuh", "seqcdc_range.cu")]
+SOURCES = [os.path.join(CSRC, f) for f in ("seqcdc.cu", "seqcdc_device.cuh", "seqcdc_range.cu", "seqcdc_dedup.cu")]
 HEADER = os.path.join(ROOT, "include", "seqcdc.h")
 
 NVCC_FLAGS = [

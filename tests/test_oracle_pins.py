@@ -318,3 +318,24 @@ def test_uniform_statistics_match_survey(avg, mean, examined):
     cuts, ex = oracle.chunk(b, oracle.table1(avg), return_examined=True)
     assert abs(b.size / cuts.size / mean - 1) < 0.02
     assert abs(ex / b.size - examined) < 0.006
+
+
+def test_fingerprint_and_dedup_definitions():
+    """The dedup oracle against closed forms: FIPS 180-4 test vectors for the
+    SHA-256 step, and a stream built from repeated blocks whose stored bytes are
+    known exactly (Eq. 1)."""
+    import hashlib
+    abc = np.frombuffer(b"abc" + b"x" * 61, dtype=np.uint8)
+    fp = oracle.fingerprints(abc, [3, 64])
+    assert fp[0].tobytes().hex() == "ba7816bf8f01cfea414140de5dae2223b00361a396177a9cb410ff61f20015ad"
+    assert fp[1].tobytes() == hashlib.sha256(b"x" * 61).digest()
+    e = oracle.fingerprints(np.zeros(0, np.uint8), [])
+    assert e.shape == (0, 32)
+    rng = np.random.default_rng(1)
+    blocks = [rng.integers(0, 256, 1000 + 7 * i).astype(np.uint8) for i in range(5)]
+    order = [0, 1, 0, 2, 1, 3, 4, 4, 0]
+    data = np.concatenate([blocks[i] for i in order])
+    cuts = np.cumsum([blocks[i].size for i in order])
+    first, uniq = oracle.dedup(data, cuts)
+    assert first.tolist() == [True, True, False, True, False, True, True, False, False]
+    assert uniq == sum(b.size for b in blocks)
