@@ -22,19 +22,32 @@ import paper_2505_21194_b200 as sc  # noqa: E402
 SM_CLOCK_GHZ = 1.965
 
 
-def sha_instr_per_block():
-    """SASS instructions in k_sha256's full-block loop (static count)."""
+ALU_PIPE = ("SHF", "LOP3", "IADD3", "VIADD", "ISETP", "SEL", "PRMT", "LEA", "FLO", "POPC", "BREV", "IABS", "VIMNMX")
+
+
+def sha_block_mix():
+    """(all, ALU-pipe) SASS instructions in k_sha256's full-block loop (static)."""
     out = subprocess.run(["cuobjdump", "-sass", sc._build.LIB], capture_output=True, text=True).stdout
-    f, addrs = False, []
+    f, lines = False, []
     for line in out.splitlines():
         if "Function :" in line:
             f = "k_sha256" in line
-        elif f and "BRA 0x" in line and "@P0" in line:
-            tgt = int(line.split("BRA 0x")[1].split()[0].rstrip(";"), 16)
-            here = int(line.split("/*")[1].split("*/")[0], 16)
-            if tgt < here:
-                addrs.append((here - tgt) // 16)
-    return max(addrs) if addrs else None
+        elif f and line.strip().startswith("/*") and "*/" in line:
+            lines.append(line)
+    # the loop: the backward branch with the largest span
+    best = None
+    for ln in lines:
+        if "BRA 0x" in ln:
+            tgt = int(ln.split("BRA 0x")[1].split()[0].rstrip(";"), 16)
+            here = int(ln.split("/*")[1].split("*/")[0], 16)
+            if tgt < here and (best is None or here - tgt > best[1] - best[0]):
+                best = (tgt, here)
+    if not best:
+        return None, None
+    body = [ln for ln in lines if best[0] <= int(ln.split("/*")[1].split("*/")[0], 16) <= best[1]]
+    ops = [ln.split("*/")[1].strip().lstrip("@!P0123456789 ").split()[0] for ln in body]
+    alu = sum(1 for o in ops if o.split(".")[0] in ALU_PIPE)
+    return len(ops), alu
 
 
 def run(cfg):
@@ -79,16 +92,18 @@ def run(cfg):
     exact = bool(np.array_equal(cuts[:k].cpu().numpy().astype(np.uint64), want_cuts))
     # the stored bytes: the oracle's set-based definition over the same chunks
     _, wuniq = oracle.dedup(b, want_cuts) if cfg == 2 else (None, None)
-    ipb = sha_instr_per_block()
-    alu_peak = 148 * 4 * SM_CLOCK_GHZ * 1e9 * 32 * 64 / ipb / 1e9 if ipb else None
+    ipb, alu = sha_block_mix()
+    # ALU pipe: one warp-instruction per 2 cycles per SMSP (rt 2, B300_MICROARCH.md)
+    alu_peak = 148 * 4 * 0.5 * SM_CLOCK_GHZ * 1e9 * 32 * 64 / alu / 1e9 if alu else None
     fp_gbs = n / t[1] / 1e6
     return {"workload": name, "bytes": n, "ncuts": k, "chunk_ms": round(t[0], 3), "fingerprint_ms": round(t[1], 3),
             "dedup_ms": round(t[2], 3), "chunk_GBps": round(n / t[0] / 1e6, 1), "fingerprint_GBps": round(fp_gbs, 1),
             "pipeline_GBps": round(n / t.sum() / 1e6, 1),
-            "fingerprint_roofline": {"bound": "alu", "sass_instr_per_64B_block": ipb,
+            "fingerprint_roofline": {"bound": "alu", "sass_instr_per_64B_block": ipb, "alu_pipe_instr_per_block": alu,
                                      "peak_GBps": round(alu_peak, 1) if alu_peak else None,
                                      "frac": round(fp_gbs / alu_peak, 3) if alu_peak else None,
-                                     "how": "148 SMs x 4 issue/clk x 1.965 GHz x 32 lanes x 64 B / instr per block"},
+                                     "how": "148 SMs x 4 SMSP x 0.5 ALU-pipe instr/clk x 1.965 GHz x 32 lanes x "
+                                            "64 B / ALU-pipe instr per block"},
             "unique_over_total": round(int(uniq.item()) / n, 6), "cuts_bit_exact": exact,
             "unique_bytes_match_oracle": (int(uniq.item()) == wuniq) if wuniq is not None else "checked in tests (scaled)",
             "oracle_s": round(time.time() - t0, 1)}
