@@ -920,7 +920,11 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int sms, int occ, Plan &pl,
                       bool single, uint64_t stop)
 {
-    const uint64_t walkers = (uint64_t)sms * occ;
+    // up to ~1.5 GiB the run ends with the longest seam extension, and 22 walkers
+    // per SM (longer segments, less contention on the tail) measured ~4% faster
+    // than 24 on config 2; larger inputs are throughput-bound (profiles/r01/sweeps.md)
+    const int occ_eff = (total <= (3ull << 29) && occ > 22 && !getenv("SEQCDC_WALKERS_PER_SM")) ? 22 : occ;
+    const uint64_t walkers = (uint64_t)sms * occ_eff;
     const uint64_t mx = p->max_size, mn = p->min_size;
     // segments per walker (x100; tuning knob) and the segment floor in max_size units
     const uint64_t spw = (uint64_t)std::max(1, env_int("SEQCDC_SEGS_PER_WALKER_X100", 100));

@@ -189,11 +189,12 @@ __device__ __forceinline__ void ring_issue(Walker &wk, uint32_t b, int lane)
     }
 #endif
     if (b0 >= wk.lo_rel && b0 + BLK <= wk.end_rel) {
+        // a whole block: one base address per side, the k*512 steps become
+        // immediate offsets of the copies (a block never wraps the ring)
+        const uint32_t dst = wk.buf + (b0 & RING_MASK) + 16 * (uint32_t)lane;
+        const uint64_t src = wk.rb + b0 + 16 * (uint32_t)lane;
 #pragma unroll
-        for (uint32_t k = 0; k < BLK / 512; k++) {
-            const uint32_t c = b0 + k * 512 + 16 * (uint32_t)lane;
-            cp_async16(wk.buf + (c & RING_MASK), wk.rb + c);
-        }
+        for (uint32_t k = 0; k < BLK / 512; k++) cp_async16(dst + k * 512, src + k * 512);
     } else if (b0 < wk.end_rel) {
 #pragma unroll 1
         for (uint32_t k = 0; k < BLK / 512; k++) {

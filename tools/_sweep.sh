@@ -1,7 +1,9 @@
 cd $GRAFT_REPO_ROOT
-for spw in 100 125 150 200 300; do
-  SEQCDC_G_FLOOR_CHUNKS=2 SEQCDC_SEGS_PER_WALKER_X100=$spw python tools/tune.py markov 2 1024 4 1 20 >> gpurun_out/sweep16.jsonl 2>&1
+for occ in 19 20 21 22 23 24; do
+  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 2 1024 4 1 30 >> gpurun_out/sweep18.jsonl 2>&1
 done
-for spw in 100 150 200; do
-  SEQCDC_G_FLOOR_CHUNKS=2 SEQCDC_SEGS_PER_WALKER_X100=$spw python tools/tune.py markov 2 4096 4 1 10 >> gpurun_out/sweep16.jsonl 2>&1
+for occ in 20 22 24; do
+  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 2 4096 4 1 10 >> gpurun_out/sweep18.jsonl 2>&1
+  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py rampmix 5 4096 8 0 10 >> gpurun_out/sweep18.jsonl 2>&1
+  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 7 2048 4 1 10 >> gpurun_out/sweep18.jsonl 2>&1
 done
