@@ -52,7 +52,20 @@ constexpr int BLK_SHIFT = SEQCDC_BLK_SHIFT;          // ring block size (log2)
 constexpr uint32_t BLK = 1u << BLK_SHIFT;
 constexpr uint32_t NBLK = SEQCDC_NBLK;               // blocks in the ring (power of two)
 constexpr uint32_t AHEAD = SEQCDC_AHEAD;             // blocks kept in flight past the window
+#ifndef SEQCDC_SPARSE
+#define SEQCDC_SPARSE 0
+#endif
+#ifndef SEQCDC_HINT_BLOCKS
+#define SEQCDC_HINT_BLOCKS 3
+#endif
+constexpr uint32_t SBLK_SHIFT = 9;                   // sparse cache: 512-byte blocks (one 16-B copy per lane)
+constexpr uint32_t SBLK = 1u << SBLK_SHIFT;
+constexpr uint32_t NS = 32;                          // sparse cache slots (16 KiB)
+#if SEQCDC_SPARSE
+constexpr uint32_t RING = SBLK * NS;
+#else
 constexpr uint32_t RING = BLK * NBLK;                // 8 KiB per walker (default geometry)
+#endif
 constexpr uint32_t RING_MASK = RING - 1;
 static_assert(AHEAD + 2 <= NBLK, "ring must hold the window's two blocks plus the lookahead");
 static_assert(BLK >= 512 && BLK % 512 == 0, "a block is whole rounds of 32 x 16-byte copies");
@@ -161,6 +174,7 @@ __device__ __forceinline__ void lt_gt_flags(uint32_t x, uint32_t y, uint32_t &lt
     gt = (~y & x) | (~(x ^ y) & u);
 }
 
+#if !SEQCDC_SPARSE
 // ------------------------------------------------------------------ the shared-memory ring
 // Software-pipelined cp.async ring: 1 KiB blocks are issued strictly in order,
 // one cp.async group each; the walk keeps exactly AHEAD groups in flight past
@@ -268,6 +282,130 @@ __device__ __forceinline__ void walker_finish(Walker &wk)
     __syncwarp();
 }
 
+// (dense ring: no hint needed, the ring streams every byte)
+__device__ __forceinline__ void ring_hint_next(Walker &, uint32_t, uint32_t, int) {}
+#else
+// ------------------------------------------------------------------ sparse (skip-aware) block cache, NEXT-2
+// Instead of streaming every byte, the walker fetches only the 512-byte blocks
+// it examines, into a direct-mapped cache of NS slots (slot = block % NS), plus
+// prefetches: the next two blocks past each window, and at each chunk start the
+// region where the NEXT chunk's scan will most likely start (anchor + min - L,
+// P:179).  The sub-minimum region of every chunk and most of each content-
+// defined skip are never read from HBM: this is the paper's skipping
+// turned into saved memory traffic.  Tags live one per lane (lane s = slot s).
+struct Walker {
+    uint64_t rb;        // absolute address of relative position 0 (cache-aligned)
+    uint32_t lo_rel;    // first loadable byte (relative)
+    uint32_t end_rel;   // end of the stream (relative, clamped to REL_CLAMP)
+    uint32_t buf;       // shared address of the cache
+    uint32_t tag;       // this lane's slot: block held (FULL = none)
+    uint32_t seq;       // this lane's slot: cp.async group that fills it
+    uint32_t gseq;      // groups committed so far (warp-uniform)
+    uint32_t ready;     // slots known to have landed (warp-uniform bit mask)
+};
+
+__device__ __forceinline__ void cache_fill(Walker &wk, uint32_t b, int lane)
+{
+    const uint32_t s = b & (NS - 1);
+    const uint32_t x0 = b << SBLK_SHIFT;
+    const uint32_t dst = wk.buf + (s << SBLK_SHIFT);
+    if (x0 >= wk.lo_rel && x0 + SBLK <= wk.end_rel) {
+        cp_async16(dst + 16 * (uint32_t)lane, wk.rb + x0 + 16 * (uint32_t)lane);
+    } else if (x0 < wk.end_rel) {
+#pragma unroll 1
+        for (uint32_t x = x0 + (uint32_t)lane; x < x0 + SBLK; x += 32)
+            if (x >= wk.lo_rel && x < wk.end_rel)
+                sts8(dst + (x - x0), *(const volatile uint8_t *)(wk.rb + x));
+    }
+    cp_async_commit();
+    if (lane == (int)s) {
+        wk.tag = b;
+        wk.seq = wk.gseq;
+    }
+    wk.gseq++;
+    wk.ready &= ~(1u << s);
+}
+
+// wait until slot s has landed (every lane committed the same groups)
+__device__ __forceinline__ void cache_wait(Walker &wk, uint32_t s)
+{
+    const uint32_t after = wk.gseq - 1 - __shfl_sync(FULL, wk.seq, s);   // groups committed after it
+    const uint32_t n = after < 7 ? after : 7;
+    cp_async_wait_n(n);
+    __syncwarp();
+    const uint32_t done = wk.gseq - 1 - n;                               // groups <= done have landed
+    wk.ready |= __ballot_sync(FULL, wk.tag != FULL && wk.seq <= done);
+}
+
+// make block b resident (warp-uniform)
+__device__ __forceinline__ void cache_need(Walker &wk, uint32_t b, int lane)
+{
+    const uint32_t s = b & (NS - 1);
+    if (__shfl_sync(FULL, wk.tag, s) != b) cache_fill(wk, b, lane);
+    if (!((wk.ready >> s) & 1u)) cache_wait(wk, s);
+}
+
+// start fetching block b unless present or its slot holds a block of the window [wl, wh]
+__device__ __forceinline__ void cache_prefetch(Walker &wk, uint32_t b, uint32_t wl, uint32_t wh, int lane)
+{
+    const uint32_t s = b & (NS - 1);
+    if (b > (wk.end_rel >> SBLK_SHIFT) || ((b - wl) & (NS - 1)) <= wh - wl) return;
+    if (__shfl_sync(FULL, wk.tag, s) != b) cache_fill(wk, b, lane);
+}
+
+// Make bytes [need_lo, need_hi) resident (need_hi - need_lo <= SBLK + 4).
+__device__ __forceinline__ void ring_need(Walker &wk, uint32_t need_lo, uint32_t need_hi, int lane)
+{
+    const uint32_t bl = need_lo >> SBLK_SHIFT, bh = (need_hi - 1) >> SBLK_SHIFT;
+    cache_need(wk, bl, lane);
+    if (bh != bl) cache_need(wk, bh, lane);
+    cache_prefetch(wk, bh + 1, bl, bh, lane);
+    cache_prefetch(wk, bh + 2, bl, bh, lane);
+}
+
+// at a chunk's first window (anchor a): prefetch where the next chunk's scan starts
+__device__ __forceinline__ void ring_hint_next(Walker &wk, uint32_t next_lo, uint32_t a, int lane)
+{
+    const uint32_t wl = a >> SBLK_SHIFT;
+    const uint32_t b0 = next_lo >> SBLK_SHIFT;
+#pragma unroll
+    for (uint32_t k = 0; k < SEQCDC_HINT_BLOCKS; k++) cache_prefetch(wk, b0 + k, wl, wl + 1, lane);
+}
+
+__device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, const DevParams &, int)
+{
+    uint32_t sb = smem_u32(smem);
+    asm volatile("mov.b32 %0, %0;" : "+r"(sb));
+    wk.buf = sb;
+    wk.rb = 0;
+    wk.lo_rel = wk.end_rel = 0;
+    wk.tag = FULL;
+    wk.seq = 0;
+    wk.gseq = 0;
+    wk.ready = 0;
+}
+
+__device__ __forceinline__ uint32_t walker_begin(Walker &wk, uint64_t a_lo, uint64_t a_end)
+{
+    cp_async_wait<0>();
+    __syncwarp();
+    wk.rb = a_lo & ~(uint64_t)RING_MASK;
+    wk.lo_rel = (uint32_t)(a_lo - wk.rb);
+    const uint64_t e = a_end > a_lo ? a_end - wk.rb : wk.lo_rel;
+    wk.end_rel = e > REL_CLAMP ? REL_CLAMP : (uint32_t)e;
+    wk.tag = FULL;
+    wk.ready = 0;
+    return wk.lo_rel;
+}
+
+__device__ __forceinline__ void walker_finish(Walker &)
+{
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
+#endif
+
 // ------------------------------------------------------------------ one chunk
 // Favourable-run mask R for M = L-1 pairs.  MSPEC = 4: exactly four (L = 5,
 // Table I); MSPEC = 0: any M <= 4 (runtime); MSPEC = -1: 5 <= M <= 15, using up
@@ -327,12 +465,17 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
     uint32_t lomask = FULL << (8 * (a & 3u));      // lane 0: pairs below the anchor
     const uint32_t qoff = 4 * (uint32_t)lane;
     const uint32_t lt_mask = lanemask_lt();
+    bool first = true;
 #pragma unroll 1
     for (;;) {
         {
             uint32_t need_hi = p0 + WIN_PAIRS + 4;
             if (need_hi > lim2 + 2) need_hi = lim2 + 2;
             ring_need(wk, p0, need_hi, lane);
+            if (first) {                           // the next chunk's scan starts near a + min - L
+                ring_hint_next(wk, a + p.mnL, p0, lane);
+                first = false;
+            }
         }
         const uint32_t q = p0 + qoff;
         const uint32_t x = lds32(wk.buf + (q & RING_MASK));

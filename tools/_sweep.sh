@@ -1,9 +1,10 @@
 cd $GRAFT_REPO_ROOT
-for occ in 19 20 21 22 23 24; do
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 2 1024 4 1 30 >> gpurun_out/sweep18.jsonl 2>&1
-done
-for occ in 20 22 24; do
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 2 4096 4 1 10 >> gpurun_out/sweep18.jsonl 2>&1
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py rampmix 5 4096 8 0 10 >> gpurun_out/sweep18.jsonl 2>&1
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 7 2048 4 1 10 >> gpurun_out/sweep18.jsonl 2>&1
+SEQCDC_LIB=build/v_sp.so python -m pytest tests/test_gpu_parity.py tests/test_gpu_range.py -m gpu -q -x > gpurun_out/pytest_sp.log 2>&1
+for v in v24 sp sph2 sph4; do
+  export SEQCDC_LIB=build/v_$v.so
+  python tools/tune.py markov 2 1024 4 1 20 >> gpurun_out/sweep19.jsonl 2>&1
+  python tools/tune.py rampmix 5 4096 8 0 10 >> gpurun_out/sweep19.jsonl 2>&1
+  python tools/tune.py uniform 1 4096 16 0 10 >> gpurun_out/sweep19.jsonl 2>&1
+  python tools/tune.py uniform 1 4096 8 0 10 >> gpurun_out/sweep19.jsonl 2>&1
+  python tools/tune.py markov 2 4096 4 1 10 >> gpurun_out/sweep19.jsonl 2>&1
 done
