@@ -500,9 +500,32 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
         if ((rmask | dmask) == 0) {                // nothing decided in this window
             need -= __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
             carry = MSPEC >= 0 ? __shfl_sync(FULL, Fm, 31) : Fm;
+            const bool flat = !__any_sync(FULL, (Fm | Om) != 0);
             p0 += WIN_PAIRS;
             lomask = FULL;
             if (p0 > lim2) return limit;
+            if (flat) {
+                // A window of equal bytes only (zero runs, constant data): neither
+                // favourable nor opposing pairs, so the counters do not
+                // move.  Gallop 512 pairs per step (16 per lane) while the bytes stay
+                // equal; resume window by window at the first step with a change.
+#pragma unroll 1
+                for (;;) {
+                    uint32_t nh = p0 + 4 * WIN_PAIRS + 4;
+                    if (nh > lim2 + 2) nh = lim2 + 2;
+                    ring_need(wk, p0, nh, lane);
+                    const uint32_t q16 = p0 + 16 * (uint32_t)lane;
+                    uint32_t wv[5];
+#pragma unroll
+                    for (int k = 0; k < 5; k++) wv[k] = lds32(wk.buf + ((q16 + 4 * k) & RING_MASK));
+                    uint32_t diff = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) diff |= wv[k] ^ __funnelshift_r(wv[k], wv[k + 1], 8);
+                    if (__any_sync(FULL, diff != 0)) break;   // (stale bytes past lim2 only cost a window)
+                    p0 += 4 * WIN_PAIRS;
+                    if (p0 > lim2) return limit;
+                }
+            }
             continue;
         }
         // per lane: byte of its first run end, byte of its k-th opposing pair

@@ -218,3 +218,31 @@ def test_stream_over_4gib():
     b = d.cpu().numpy()
     del d
     _assert_same(got, oracle.chunk(b, p), "4 GiB+")
+
+
+def _flat_runs_stream(rng, n):
+    """Random pieces separated by runs of one repeated byte (length 1..6000):
+    exercises the walker's equal-bytes gallop entering/leaving at every offset."""
+    out, tot = [], 0
+    while tot < n:
+        if rng.random() < 0.5:
+            ln = int(rng.integers(1, 6000))
+            piece = np.full(ln, int(rng.integers(0, 256)), np.uint8)
+        else:
+            ln = int(rng.integers(1, 3000))
+            piece = rng.integers(0, int(rng.choice([3, 256])), ln).astype(np.uint8)
+        out.append(piece)
+        tot += ln
+    return np.concatenate(out)[:n]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_flat_runs_gallop(seed):
+    rng = np.random.default_rng(seed)
+    b = _flat_runs_stream(rng, 3 << 20)
+    for p in (oracle.table1(4), oracle.table1(8, 1), oracle.table1(16), oracle.Params(0, 3, 2, 5, 100, 700),
+              oracle.Params(1, 6, 9, 0, 64, 5000)):
+        _assert_same(_gpu_chunk(b, p), oracle.chunk(b, p), f"flat runs {p}")
+    sc.set_segment_bytes(1 << 16)
+    p = oracle.table1(4)
+    _assert_same(_gpu_chunk(b, p), oracle.chunk(b, p), "flat runs, 64 KiB segments")
