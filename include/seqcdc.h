@@ -59,6 +59,10 @@ extern "C" {
 #define SEQCDC_DECREASING 1
 #define SEQCDC_MAX_SEQ_LENGTH 16   /* implementation limit on SeqLength */
 
+/* seqcdc_params_t.flags: compare bytes as SIGNED int8 instead of unsigned
+ * (the alternative reading of P:215's untyped mm512_cmpgt; DESIGN.md c6). */
+#define SEQCDC_FLAG_SIGNED 1u
+
 /* Written to *d_ncuts if the device detects inconsistent batch offsets
  * (non-monotone, or d_offsets[ns]-d_offsets[0] != total_bytes). */
 #define SEQCDC_NCUTS_BAD_INPUT UINT64_MAX
@@ -73,13 +77,13 @@ typedef struct seqcdc_params {
                                byte; 0 disables skipping                    */
     uint64_t min_size;      /* >= L; scanning starts at chunk start + min - L */
     uint64_t max_size;      /* >= min_size; forced cut                        */
-    uint32_t flags;         /* reserved, must be 0                                   */
+    uint32_t flags;         /* 0, or SEQCDC_FLAG_SIGNED                              */
     uint32_t reserved;      /* must be 0                                             */
 } seqcdc_params_t;
 
 /* SEQCDC_OK if *p is acceptable, SEQCDC_EINVAL otherwise (mode not 0/1,
- * L < 2 or L > SEQCDC_MAX_SEQ_LENGTH, T == 0, min < L, max < min, flags or
- * reserved != 0, p == NULL). */
+ * L < 2 or L > SEQCDC_MAX_SEQ_LENGTH, T == 0, min < L, max < min, unknown
+ * flags, reserved != 0, p == NULL). */
 int seqcdc_validate_params(const seqcdc_params_t *p);
 
 /* Table I row for avg_kib in {4, 8, 16} with min = avg/2 and

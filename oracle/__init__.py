@@ -47,6 +47,7 @@ class Params:
     skip_size: int = 256            # S, bytes skipped; 0 disables skipping
     min_size: int = 4096
     max_size: int = 16384
+    signed: bool = False            # compare bytes as int8 (reading c6's alternative)
 
     def check(self) -> None:
         if self.mode not in (0, 1):
@@ -86,11 +87,11 @@ def _load():
         lib = ctypes.CDLL(build())
         u64, u32, p = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p
         lib.oracle_chunk.restype = ctypes.c_int64
-        lib.oracle_chunk.argtypes = [p, u64, u32, u32, u32, u32, u64, u64, p, u64, p]
+        lib.oracle_chunk.argtypes = [p, u64, u32, u32, u32, u32, u64, u64, u32, p, u64, p]
         lib.oracle_next_cut.restype = u64
-        lib.oracle_next_cut.argtypes = [p, u64, u64, u32, u32, u32, u32, u64, u64, p]
+        lib.oracle_next_cut.argtypes = [p, u64, u64, u32, u32, u32, u32, u64, u64, u32, p]
         lib.oracle_chunk_batch.restype = ctypes.c_int64
-        lib.oracle_chunk_batch.argtypes = [p, p, u32, u32, u32, u32, u32, u64, u64, p, u64, p]
+        lib.oracle_chunk_batch.argtypes = [p, p, u32, u32, u32, u32, u32, u64, u64, u32, p, u64, p]
         _lib = lib
     return _lib
 
@@ -115,7 +116,7 @@ def chunk(data, p: Params, return_examined: bool = False):
     cuts = np.empty(cap, dtype=np.uint64)
     ex = ctypes.c_uint64(0)
     k = _load().oracle_chunk(b.ctypes.data, n, p.mode, p.seq_length, p.skip_trigger,
-                             p.skip_size, p.min_size, p.max_size, cuts.ctypes.data, cap,
+                             p.skip_size, p.min_size, p.max_size, int(p.signed), cuts.ctypes.data, cap,
                              ctypes.addressof(ex))
     if k < 0:
         raise RuntimeError(f"oracle_chunk failed ({k})")
@@ -130,7 +131,7 @@ def next_cut(data, base: int, p: Params) -> int:
         raise ValueError("base out of range")
     return int(_load().oracle_next_cut(b.ctypes.data, b.size, base, p.mode, p.seq_length,
                                        p.skip_trigger, p.skip_size, p.min_size, p.max_size,
-                                       None))
+                                       int(p.signed), None))
 
 
 def chunk_batch(data, offsets, p: Params):
@@ -144,7 +145,7 @@ def chunk_batch(data, offsets, p: Params):
     idx = np.empty(ns + 1, dtype=np.uint64)
     k = _load().oracle_chunk_batch(b.ctypes.data, off.ctypes.data, ns, p.mode, p.seq_length,
                                    p.skip_trigger, p.skip_size, p.min_size, p.max_size,
-                                   cuts.ctypes.data, cap, idx.ctypes.data)
+                                   int(p.signed), cuts.ctypes.data, cap, idx.ctypes.data)
     if k < 0:
         raise RuntimeError(f"oracle_chunk_batch failed ({k})")
     return cuts[:k].copy(), idx
@@ -168,6 +169,8 @@ def chunk_py(data, p: Params) -> list:
                 cut = limit
                 break
             x, y = b[i], b[i + 1]
+            if p.signed:                               # int8 order
+                x, y = (x ^ 0x80) - 128, (y ^ 0x80) - 128
             fav = x < y if p.mode == INCREASING else x > y
             opn = x > y if p.mode == INCREASING else x < y
             if fav:
@@ -203,7 +206,7 @@ def chunk_py(data, p: Params) -> list:
 # --------------------------------------------------------------------------
 def chunk_query(data, p: Params) -> np.ndarray:
     p.check()
-    b = _as_u8(data).astype(np.int16)
+    b = _as_u8(data).view(np.int8).astype(np.int16) if p.signed else _as_u8(data).astype(np.int16)
     n = int(b.size)
     L, T, S = p.seq_length, p.skip_trigger, p.skip_size
     if n == 0:

@@ -33,7 +33,8 @@
  * the second byte of the triggering pair, i.e. at d+1+S (c3); both counters
  * reset at chunk start and after a skip, the run also resets on any
  * non-favourable pair (c4); equal bytes set neither flag (c5); bytes compare
- * as UNSIGNED (c6); skipped bytes count toward max and a skip landing past the
+ * as UNSIGNED (c6; `sgn` = 1 selects the signed reading, P:215's
+ * mm512_cmpgt without a type suffix could be the signed epi8 compare); skipped bytes count toward max and a skip landing past the
  * limit gives the limit (c8); the last chunk may be shorter than min and the
  * last cut is n; n == 0 gives no cuts (c9).
  *
@@ -68,7 +69,7 @@ int oracle_check_params(uint32_t mode, uint32_t seq_length, uint32_t skip_trigge
 uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
                          uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
                          uint32_t skip_size, uint64_t min_size, uint64_t max_size,
-                         uint64_t *examined)
+                         uint32_t sgn, uint64_t *examined)
 {
     uint64_t limit = base + max_size;              /* P:266 max forced cut */
     if (limit > n) limit = n;                      /* end of stream (c9) */
@@ -77,7 +78,8 @@ uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
     uint32_t opp = 0;                              /* opposing pairs since reset */
     for (;;) {
         if (i + 1 >= limit) return limit;          /* no pair (i, i+1) left */
-        uint8_t x = b[i], y = b[i + 1];            /* unsigned bytes (c6) */
+        int x = sgn ? (int)(int8_t)b[i] : (int)b[i];          /* unsigned bytes (c6) */
+        int y = sgn ? (int)(int8_t)b[i + 1] : (int)b[i + 1];  /* or signed (flag)    */
         if (examined) (*examined)++;
         int favourable, opposing;
         if (mode == 0) { favourable = x < y; opposing = x > y; }   /* Increasing */
@@ -111,14 +113,14 @@ uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
 int64_t oracle_chunk(const uint8_t *b, uint64_t n,
                      uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
                      uint32_t skip_size, uint64_t min_size, uint64_t max_size,
-                     uint64_t *cuts, uint64_t cap, uint64_t *examined)
+                     uint32_t sgn, uint64_t *cuts, uint64_t cap, uint64_t *examined)
 {
     if (oracle_check_params(mode, seq_length, skip_trigger, min_size, max_size))
         return -ORACLE_EINVAL;
     uint64_t k = 0, base = 0;
     while (base < n) {
         uint64_t c = oracle_next_cut(b, n, base, mode, seq_length, skip_trigger,
-                                     skip_size, min_size, max_size, examined);
+                                     skip_size, min_size, max_size, sgn, examined);
         if (k >= cap) return -ORACLE_ECAP;
         cuts[k++] = c;
         base = c;
@@ -135,14 +137,14 @@ int64_t oracle_chunk(const uint8_t *b, uint64_t n,
 int64_t oracle_chunk_batch(const uint8_t *b, const uint64_t *offsets, uint32_t ns,
                            uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
                            uint32_t skip_size, uint64_t min_size, uint64_t max_size,
-                           uint64_t *cuts, uint64_t cap, uint64_t *cut_index)
+                           uint32_t sgn, uint64_t *cuts, uint64_t cap, uint64_t *cut_index)
 {
     uint64_t total = 0;
     for (uint32_t j = 0; j < ns; j++) {
         cut_index[j] = total;
         uint64_t lo = offsets[j], hi = offsets[j + 1];
         int64_t k = oracle_chunk(b + lo, hi - lo, mode, seq_length, skip_trigger, skip_size,
-                                 min_size, max_size, cuts + total, cap - total, NULL);
+                                 min_size, max_size, sgn, cuts + total, cap - total, NULL);
         if (k < 0) return k;
         for (int64_t q = 0; q < k; q++) cuts[total + q] += lo;
         total += (uint64_t)k;

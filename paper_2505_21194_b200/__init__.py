@@ -20,6 +20,7 @@ from . import _build
 
 INCREASING = 0
 DECREASING = 1
+FLAG_SIGNED = 1
 
 SEQCDC_OK, SEQCDC_EINVAL, SEQCDC_ENOMEM, SEQCDC_ECUDA = 0, 1, 2, 3
 NCUTS_BAD_INPUT = (1 << 64) - 1
@@ -51,10 +52,11 @@ class SeqParams:
     skip_size: int = 256
     min_size: int = 4096
     max_size: int = 16384
+    flags: int = 0          # SEQCDC_FLAG_SIGNED (1): int8 byte order
 
     def c(self) -> _CParams:
         return _CParams(self.mode, self.seq_length, self.skip_trigger, self.skip_size,
-                        self.min_size, self.max_size, 0, 0)
+                        self.min_size, self.max_size, self.flags, 0)
 
     @staticmethod
     def table1(avg_kib: int, mode: int = INCREASING) -> "SeqParams":

@@ -1073,6 +1073,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.p.mn = (uint32_t)p->min_size;
     w.p.mx = (uint32_t)p->max_size;
     w.p.mnL = (uint32_t)p->min_size - p->seq_length;
+    w.p.xm = (p->flags & SEQCDC_FLAG_SIGNED) ? 0x80808080u : 0u;
     w.p.bs = geo.bs;
     w.p.nb = geo.nb;
     w.p.ah = geo.ah;
@@ -1193,7 +1194,7 @@ SEQCDC_API int seqcdc_validate_params(const seqcdc_params_t *p)
     if (p->min_size < p->seq_length) return SEQCDC_EINVAL;
     if (p->max_size < p->min_size) return SEQCDC_EINVAL;
     if (p->max_size > (1ull << 28)) return SEQCDC_EINVAL;  // implementation limit: 256 MiB chunks
-    if (p->flags || p->reserved) return SEQCDC_EINVAL;
+    if ((p->flags & ~SEQCDC_FLAG_SIGNED) || p->reserved) return SEQCDC_EINVAL;
     return SEQCDC_OK;
 }
 

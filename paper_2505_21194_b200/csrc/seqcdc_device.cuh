@@ -80,6 +80,7 @@ struct DevParams {
     uint32_t L, T, S, M;   // M = L-1 favourable pairs per run
     uint32_t mn, mx;       // min/max chunk sizes (<= 2^28, validated on the host)
     uint32_t mnL;          // mn - L: offset of the scan anchor from the chunk start
+    uint32_t xm;           // 0x80808080 for the signed-byte reading (flag), else 0
     uint32_t bs, nb, ah;   // ring geometry (reported; compile-time in this build)
 };
 
@@ -478,8 +479,9 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
             }
         }
         const uint32_t q = p0 + qoff;
-        const uint32_t x = lds32(wk.buf + (q & RING_MASK));
-        const uint32_t xn = lds32(wk.buf + ((q + 4) & RING_MASK));
+        // (signed reading: flipping bit 7 of every byte maps int8 order onto uint8 order)
+        const uint32_t x = lds32(wk.buf + (q & RING_MASK)) ^ p.xm;
+        const uint32_t xn = lds32(wk.buf + ((q + 4) & RING_MASK)) ^ p.xm;
         const uint32_t y = __funnelshift_r(x, xn, 8);     // y_k = byte q+k+1
         uint32_t lt, gt;
         lt_gt_flags(x, y, lt, gt);

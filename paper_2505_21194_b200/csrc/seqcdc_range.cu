@@ -182,6 +182,7 @@ SEQCDC_API int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint6
     a.p.mn = (uint32_t)p->min_size;
     a.p.mx = (uint32_t)p->max_size;
     a.p.mnL = (uint32_t)p->min_size - p->seq_length;
+    a.p.xm = (p->flags & SEQCDC_FLAG_SIGNED) ? 0x80808080u : 0u;
     seqcdc_ring_geometry(p, &a.p.bs, &a.p.nb, &a.p.ah);
     const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
     if (p->mode == SEQCDC_INCREASING) {

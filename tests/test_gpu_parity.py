@@ -19,7 +19,8 @@ import paper_2505_21194_b200 as sc  # noqa: E402
 
 def _sp(p: oracle.Params) -> sc.SeqParams:
     # the two sides keep separate parameter types on purpose (no shared code)
-    return sc.SeqParams(p.mode, p.seq_length, p.skip_trigger, p.skip_size, p.min_size, p.max_size)
+    return sc.SeqParams(p.mode, p.seq_length, p.skip_trigger, p.skip_size, p.min_size, p.max_size,
+                        sc.FLAG_SIGNED if p.signed else 0)
 
 
 def _dev(b: np.ndarray):
@@ -246,3 +247,23 @@ def test_flat_runs_gallop(seed):
     sc.set_segment_bytes(1 << 16)
     p = oracle.table1(4)
     _assert_same(_gpu_chunk(b, p), oracle.chunk(b, p), "flat runs, 64 KiB segments")
+
+
+@pytest.mark.parametrize("kind,seed", [("uniform", 41), ("markov", 42), ("rampmix", 43)])
+def test_signed_flag(kind, seed):
+    """SEQCDC_FLAG_SIGNED (int8 byte order, DESIGN.md c6 alternative) against the
+    oracle's signed reading, single stream and batch."""
+    import dataclasses
+    b = synth.fill_host(kind, seed, 0, 6 << 20)
+    for p0 in (oracle.table1(8), oracle.table1(4, 1), oracle.Params(0, 3, 4, 9, 40, 400)):
+        p = dataclasses.replace(p0, signed=True)
+        want = oracle.chunk(b, p)
+        _assert_same(_gpu_chunk(b, p), want, f"signed {p}")
+        if kind == "uniform":          # (Markov text is 7-bit ASCII: both orders agree there)
+            assert not np.array_equal(want, oracle.chunk(b, p0))
+    offs = np.array([0, 1000, 500000, 2 << 20, 6 << 20], np.uint64)
+    p = dataclasses.replace(oracle.table1(8), signed=True)
+    wc, wi = oracle.chunk_batch(b, offs, p)
+    gc, gi = _gpu_batch(b, offs, p)
+    _assert_same(gi, wi, "signed batch index")
+    _assert_same(gc, wc, "signed batch")

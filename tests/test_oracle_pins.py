@@ -339,3 +339,35 @@ def test_fingerprint_and_dedup_definitions():
     first, uniq = oracle.dedup(data, cuts)
     assert first.tolist() == [True, True, False, True, False, True, True, False, False]
     assert uniq == sum(b.size for b in blocks)
+
+
+def test_signed_reading_is_unsigned_on_flipped_bytes():
+    """Flag for reading c6's alternative (signed int8 compares): a signed compare
+    of x and y orders exactly like an unsigned compare of x^0x80 and y^0x80, so
+    the signed oracle on b must equal the unsigned oracle on b^0x80 (closed form),
+    and the three formulations agree under the flag."""
+    rng = np.random.default_rng(11)
+    for trial in range(200):
+        n = int(rng.integers(0, 3000))
+        b = rng.integers(0, 256, n).astype(np.uint8)
+        L = int(rng.integers(2, 7))
+        mn = int(rng.integers(L, L + 60))
+        p = oracle.Params(int(rng.integers(0, 2)), L, int(rng.integers(1, 40)), int(rng.integers(0, 90)), mn,
+                          int(rng.integers(mn, mn + 300)), True)
+        pu = oracle.Params(p.mode, p.seq_length, p.skip_trigger, p.skip_size, p.min_size, p.max_size, False)
+        want = oracle.chunk(b ^ np.uint8(0x80), pu)
+        assert np.array_equal(oracle.chunk(b, p), want)
+        if n <= 600:
+            assert oracle.chunk_py(b, p) == want.tolist()
+            assert np.array_equal(oracle.chunk_query(b, p), want)
+
+
+def test_fig3_block_signed_reading(golden):
+    """Under the signed reading the Fig. 3-consistent block cuts at
+    63 instead of 64: AF/F0 are negative as int8, so the filler's F0 -> 12 step is
+    increasing (SURVEY [MC-7]; filler-dependent, which is why c6 stays unsigned)."""
+    g = golden("fig3_block.txt")
+    b = np.array([int(x, 16) for x in g["bytes"]], np.uint8)
+    p = oracle.Params(int(g["mode"][0]), int(g["seq_length"][0]), int(g["skip_trigger"][0]),
+                      int(g["skip_size"][0]), int(g["min_size"][0]), int(g["max_size"][0]), True)
+    assert int(oracle.chunk(b, p)[0]) == 63
