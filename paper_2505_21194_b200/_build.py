@@ -31,13 +31,29 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu to an object in parallel, then link libseqcdc.so."""
     if not (force or stale()):
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
+    from concurrent.futures import ThreadPoolExecutor
     cu = [s for s in sources() if s.endswith(".cu")]
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", tmp, *cu]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+    objs = [os.path.join(CSRC, os.path.basename(c)[:-3] + f".{os.getpid()}.o") for c in cu]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def comp(pair):
+        src, obj = pair
+        cmd = ["nvcc", *compile_flags, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
+
+    try:
+        with ThreadPoolExecutor(len(cu)) as ex:
+            list(ex.map(comp, zip(cu, objs)))
+        tmp = LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
+        os.replace(tmp, LIB)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     return LIB

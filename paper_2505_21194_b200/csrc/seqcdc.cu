@@ -862,6 +862,14 @@ static void set_attrs()
     cudaFuncSetAttribute((const void *)k_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 20 * STITCH_MAX_SEGS);
 }
 
+template <int MODE>
+static void set_attrs_mode()
+{
+    set_attrs<MODE, 4>();
+    set_attrs<MODE, 0>();
+    set_attrs<MODE, -1>();
+}
+
 static int env_int(const char *name, int dflt)
 {
     const char *e = getenv(name);
@@ -890,12 +898,10 @@ static int device_info(int &sms, int &occ, uint32_t smem = 0)
         if (cudaGetDevice(&dev) != cudaSuccess) return SEQCDC_ECUDA;
         int nsm = 0;
         if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return SEQCDC_ECUDA;
-        set_attrs<0, 4>();
-        set_attrs<0, 0>();
-        set_attrs<0, -1>();
-        set_attrs<1, 4>();
-        set_attrs<1, 0>();
-        set_attrs<1, -1>();
+        set_attrs_mode<0>();
+        set_attrs_mode<1>();
+        set_attrs_mode<2>();
+        set_attrs_mode<3>();
         g_sms = nsm;
     }
     const uint32_t key = std::min<uint32_t>(smem / 1024, 65);
@@ -1046,6 +1052,14 @@ static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, 
     k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
 }
 
+template <int MODE>
+static void launch_ms(int ms, const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
+{
+    if (ms == 4) launch_all<MODE, 4>(w, pl, sms, st, pr);
+    else if (ms == 0) launch_all<MODE, 0>(w, pl, sms, st, pr);
+    else launch_all<MODE, -1>(w, pl, sms, st, pr);
+}
+
 static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total, uint64_t stop,
                uint64_t out_add, const seqcdc_params_t *p, const DevParams &geo, uint64_t *d_cuts, uint64_t *d_cut_index,
                uint64_t *d_ncuts, uint8_t *ws, size_t ws_bytes, const Plan &pl, int sms, cudaStream_t st,
@@ -1073,7 +1087,6 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.p.mn = (uint32_t)p->min_size;
     w.p.mx = (uint32_t)p->max_size;
     w.p.mnL = (uint32_t)p->min_size - p->seq_length;
-    w.p.xm = (p->flags & SEQCDC_FLAG_SIGNED) ? 0x80808080u : 0u;
     w.p.bs = geo.bs;
     w.p.nb = geo.nb;
     w.p.ah = geo.ah;
@@ -1117,14 +1130,12 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
         k_setup<<<1, 1024, 0, st>>>(w);
     }
     const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
-    if (p->mode == SEQCDC_INCREASING) {
-        if (ms == 4) launch_all<0, 4>(w, pl, sms, st, pr);
-        else if (ms == 0) launch_all<0, 0>(w, pl, sms, st, pr);
-        else launch_all<0, -1>(w, pl, sms, st, pr);
-    } else {
-        if (ms == 4) launch_all<1, 4>(w, pl, sms, st, pr);
-        else if (ms == 0) launch_all<1, 0>(w, pl, sms, st, pr);
-        else launch_all<1, -1>(w, pl, sms, st, pr);
+    // MODE: bit 0 = Decreasing, bit 1 = signed-byte reading (flag)
+    switch (p->mode | ((p->flags & SEQCDC_FLAG_SIGNED) ? 2u : 0u)) {
+    case 0: launch_ms<0>(ms, w, pl, sms, st, pr); break;
+    case 1: launch_ms<1>(ms, w, pl, sms, st, pr); break;
+    case 2: launch_ms<2>(ms, w, pl, sms, st, pr); break;
+    default: launch_ms<3>(ms, w, pl, sms, st, pr); break;
     }
     prof_mark(pr, 3, st);
     if (pr) {

@@ -80,7 +80,6 @@ struct DevParams {
     uint32_t L, T, S, M;   // M = L-1 favourable pairs per run
     uint32_t mn, mx;       // min/max chunk sizes (<= 2^28, validated on the host)
     uint32_t mnL;          // mn - L: offset of the scan anchor from the chunk start
-    uint32_t xm;           // 0x80808080 for the signed-byte reading (flag), else 0
     uint32_t bs, nb, ah;   // ring geometry (reported; compile-time in this build)
 };
 
@@ -479,9 +478,11 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
             }
         }
         const uint32_t q = p0 + qoff;
-        // (signed reading: flipping bit 7 of every byte maps int8 order onto uint8 order)
-        const uint32_t x = lds32(wk.buf + (q & RING_MASK)) ^ p.xm;
-        const uint32_t xn = lds32(wk.buf + ((q + 4) & RING_MASK)) ^ p.xm;
+        // MODE bit 0: Decreasing; bit 1: signed reading (flipping bit 7 of every
+        // byte maps int8 order onto uint8 order)
+        constexpr uint32_t XM = (MODE & 2) ? H : 0u;
+        const uint32_t x = lds32(wk.buf + (q & RING_MASK)) ^ XM;
+        const uint32_t xn = lds32(wk.buf + ((q + 4) & RING_MASK)) ^ XM;
         const uint32_t y = __funnelshift_r(x, xn, 8);     // y_k = byte q+k+1
         uint32_t lt, gt;
         lt_gt_flags(x, y, lt, gt);
@@ -490,8 +491,8 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
         // below (events are taken in pair order, so a stale one can only come after
         // every valid one).
         const uint32_t V = (lane ? FULL : lomask) & H;
-        const uint32_t Fm = (MODE == 0 ? lt : gt) & V;
-        const uint32_t Om = (MODE == 0 ? gt : lt) & V;
+        const uint32_t Fm = ((MODE & 1) == 0 ? lt : gt) & V;
+        const uint32_t Om = ((MODE & 1) == 0 ? gt : lt) & V;
         const uint32_t R = run_mask<MSPEC>(Fm, carry, p.M, lane);
         const uint32_t cnt = __popc(Om);
         const uint32_t b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),

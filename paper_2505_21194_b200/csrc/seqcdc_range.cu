@@ -145,6 +145,14 @@ void launch(const ResyncArgs &a, cudaStream_t st)
     k_resync_tail<<<148, 256, 0, st>>>(a);
 }
 
+template <int MODE>
+void launch_ms(int ms, const ResyncArgs &a, cudaStream_t st)
+{
+    if (ms == 4) launch<MODE, 4>(a, st);
+    else if (ms == 0) launch<MODE, 0>(a, st);
+    else launch<MODE, -1>(a, st);
+}
+
 }  // namespace
 }  // namespace seqcdc
 
@@ -182,17 +190,13 @@ SEQCDC_API int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint6
     a.p.mn = (uint32_t)p->min_size;
     a.p.mx = (uint32_t)p->max_size;
     a.p.mnL = (uint32_t)p->min_size - p->seq_length;
-    a.p.xm = (p->flags & SEQCDC_FLAG_SIGNED) ? 0x80808080u : 0u;
     seqcdc_ring_geometry(p, &a.p.bs, &a.p.nb, &a.p.ah);
     const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
-    if (p->mode == SEQCDC_INCREASING) {
-        if (ms == 4) launch<0, 4>(a, st);
-        else if (ms == 0) launch<0, 0>(a, st);
-        else launch<0, -1>(a, st);
-    } else {
-        if (ms == 4) launch<1, 4>(a, st);
-        else if (ms == 0) launch<1, 0>(a, st);
-        else launch<1, -1>(a, st);
+    switch (p->mode | ((p->flags & SEQCDC_FLAG_SIGNED) ? 2u : 0u)) {
+    case 0: launch_ms<0>(ms, a, st); break;
+    case 1: launch_ms<1>(ms, a, st); break;
+    case 2: launch_ms<2>(ms, a, st); break;
+    default: launch_ms<3>(ms, a, st); break;
     }
     return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
 }

@@ -1,8 +1,5 @@
 cd $GRAFT_REPO_ROOT
-for occ in 6 8 12 16 24; do
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py uniform 1 4096 16 0 10 >> gpurun_out/sweep21.jsonl 2>&1
-  SEQCDC_WALKERS_PER_SM=$occ python tools/tune.py markov 2 4096 16 1 10 >> gpurun_out/sweep21.jsonl 2>&1
-done
-for fl in 32 64 128 256; do
-  SEQCDC_G_FLOOR_CHUNKS=$fl python tools/tune.py uniform 1 4096 16 0 10 >> gpurun_out/sweep21.jsonl 2>&1
-done
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_range.py -m gpu -q -x > gpurun_out/pytest_quick.log 2>&1
+for i in 1 2; do python tools/tune.py markov 2 1024 4 1 30 >> gpurun_out/sweep22.jsonl 2>&1; done
+SEQCDC_WALKERS_PER_SM=1 python tools/tune.py markov 2 64 4 1 5 >> gpurun_out/sweep22.jsonl 2>&1
+python tools/tune.py markov 2 4096 4 1 10 >> gpurun_out/sweep22.jsonl 2>&1
