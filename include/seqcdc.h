@@ -179,6 +179,18 @@ int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_l
                         uint64_t *d_status, void *stream);
 
 /*
+ * seqcdc_range_resync_dev: the same, with the true entry read on the device
+ * from *d_entry as a GLOBAL offset (e.g. straight out of an NCCL all_gather of
+ * the overhangs), so the whole exchange can be enqueued without a host sync.
+ * An entry before the range is clamped to its start, one at or past the range
+ * end gives 0 cuts (d_status[0] = 2, d_status[3] = the entry).
+ */
+int seqcdc_range_resync_dev(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
+                            const uint64_t *d_entry, uint64_t global_offset, const seqcdc_params_t *p,
+                            const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts,
+                            uint64_t *d_ncuts, uint64_t *d_status, void *stream);
+
+/*
  * After chunking (§2): "Each data
  * chunk is hashed using a collision-resistant hashing algorithm, such as
  * SHA-256 ... to obtain a fingerprint"; "the fingerprint is compared

@@ -30,7 +30,7 @@ EXPORTS = (
     "seqcdc_validate_params", "seqcdc_default_params", "seqcdc_max_cuts", "seqcdc_max_cuts_batch",
     "seqcdc_workspace_size", "seqcdc_chunk", "seqcdc_chunk_batch", "seqcdc_strerror",
     "seqcdc_build_info", "seqcdc_set_segment_bytes", "seqcdc_profile_enable", "seqcdc_profile_collect",
-    "seqcdc_range_max_cuts", "seqcdc_range_chunk", "seqcdc_range_resync",
+    "seqcdc_range_max_cuts", "seqcdc_range_chunk", "seqcdc_range_resync", "seqcdc_range_resync_dev",
     "seqcdc_fingerprint", "seqcdc_dedup_workspace_size", "seqcdc_dedup",
 )
 
@@ -114,6 +114,8 @@ def lib():
         L.seqcdc_range_chunk.restype = ctypes.c_int
         L.seqcdc_range_resync.argtypes = [p, u64, u64, u64, u64, P, p, p, p, p, p, p]
         L.seqcdc_range_resync.restype = ctypes.c_int
+        L.seqcdc_range_resync_dev.argtypes = [p, u64, u64, p, u64, P, p, p, p, p, p, p]
+        L.seqcdc_range_resync_dev.restype = ctypes.c_int
         L.seqcdc_fingerprint.argtypes = [p, p, p, u64, p, p]
         L.seqcdc_fingerprint.restype = ctypes.c_int
         L.seqcdc_dedup_workspace_size.argtypes = [u64]
@@ -308,3 +310,17 @@ def dedup_into(digests, cuts, ncuts, unique_bytes, first=None, max_cuts=None, wo
 
 def dedup_workspace_size(max_cuts: int) -> int:
     return int(lib().seqcdc_dedup_workspace_size(int(max_cuts)))
+
+
+def range_resync_dev_into(buf, range_len: int, d_entry, global_offset: int, p: SeqParams, spec, spec_n, cuts, ncuts,
+                          status, stream=None) -> None:
+    """Asynchronous seqcdc_range_resync_dev: the entry (a global offset) is read on
+    the device from ``d_entry`` (an int64 CUDA tensor element), no host sync."""
+    _require_cuda(buf, "buf")
+    cp = p.c()
+    rc = lib().seqcdc_range_resync_dev(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len,
+                                       d_entry.data_ptr(), global_offset, ctypes.byref(cp),
+                                       spec.data_ptr() if spec.numel() else None, spec_n.data_ptr(),
+                                       cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(),
+                                       status.data_ptr(), _stream_ptr(stream, buf.device))
+    _check(rc, "seqcdc_range_resync_dev")

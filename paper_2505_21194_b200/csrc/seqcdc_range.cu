@@ -33,6 +33,7 @@ enum { ST_MERGED = 0, ST_M = 1, ST_J = 2, ST_OVERHANG = 3 };
 struct ResyncArgs {
     const uint8_t *buf;
     uint64_t buf_len, stop, entry, gofs;
+    const uint64_t *d_entry;  // if set: the entry as a GLOBAL offset, read on the device
     const uint64_t *spec;     // speculative cut list (global offsets, ascending)
     const uint64_t *spec_n;   // its length (device)
     uint64_t *out, *ncuts, *status;
@@ -76,12 +77,27 @@ __global__ void __launch_bounds__(32) k_resync(ResyncArgs a)
     Walker wk;
     walker_init(wk, ring, a.p, lane);
     const uint64_t abase = (uint64_t)(uintptr_t)a.buf;
+    uint64_t entry = a.entry;
+    if (a.d_entry) {              // device-side entry: the predecessor's overhang (global)
+        const uint64_t g = *a.d_entry;
+        entry = g < a.gofs ? 0 : (g - a.gofs > a.stop ? a.stop : g - a.gofs);
+    }
+    if (entry >= a.stop) {        // no chunk starts in the range
+        if (lane == 0) {
+            *a.ncuts = 0;
+            a.status[ST_MERGED] = 2;                    // 2 = empty (k_resync_tail leaves it alone)
+            a.status[ST_M] = 0;
+            a.status[ST_J] = 0;
+            a.status[ST_OVERHANG] = a.gofs + entry;
+        }
+        return;
+    }
     Spec sp{0, *a.spec_n, 0, 0};
     spec_load(a, sp, lane);
     uint64_t vbuf = 0;            // 32 output cuts buffered in lanes
     uint32_t m = 0;
     int64_t j = -1;
-    uint64_t pos = a.entry, last = a.entry;
+    uint64_t pos = entry, last = entry;
 #pragma unroll 1
     while (pos < a.stop && j < 0) {
         uint32_t base = walker_begin(wk, abase + pos, abase + a.buf_len);
@@ -117,6 +133,7 @@ __global__ void __launch_bounds__(32) k_resync(ResyncArgs a)
 __global__ void __launch_bounds__(256) k_resync_tail(ResyncArgs a)
 {
     const uint64_t merged = a.status[ST_MERGED], m = a.status[ST_M];
+    if (merged == 2) return;                          // empty range (written by k_resync)
     const uint64_t k = *a.spec_n;
     const uint64_t j = a.status[ST_J];
     const uint64_t ns = merged ? k - (j + 1) : 0;
@@ -158,15 +175,39 @@ void launch_ms(int ms, const ResyncArgs &a, cudaStream_t st)
 
 using namespace seqcdc;
 
+static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                       const uint64_t *d_entry, uint64_t global_offset, const seqcdc_params_t *p,
+                       const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
+                       uint64_t *d_status, void *stream);
+
+SEQCDC_API int seqcdc_range_resync_dev(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
+                                       const uint64_t *d_entry, uint64_t global_offset, const seqcdc_params_t *p,
+                                       const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts,
+                                       uint64_t *d_ncuts, uint64_t *d_status, void *stream)
+{
+    if (!d_entry) return SEQCDC_EINVAL;
+    return resync_impl(d_buf, buf_len, range_len, 0, d_entry, global_offset, p, d_spec, d_spec_n, d_cuts, d_ncuts,
+                       d_status, stream);
+}
+
 SEQCDC_API int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
                                    uint64_t global_offset, const seqcdc_params_t *p, const uint64_t *d_spec,
                                    const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
                                    uint64_t *d_status, void *stream)
 {
+    return resync_impl(d_buf, buf_len, range_len, entry, nullptr, global_offset, p, d_spec, d_spec_n, d_cuts,
+                       d_ncuts, d_status, stream);
+}
+
+static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                       const uint64_t *d_entry, uint64_t global_offset, const seqcdc_params_t *p,
+                       const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
+                       uint64_t *d_status, void *stream)
+{
     if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
     if (!d_ncuts || !d_status || !d_spec_n || range_len > buf_len || entry > range_len) return SEQCDC_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    if (entry >= range_len) {
+    if (!d_entry && entry >= range_len) {
         k_resync_empty<<<1, 1, 0, st>>>(d_ncuts, d_status, global_offset + entry);
         return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
     }
@@ -177,6 +218,7 @@ SEQCDC_API int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint6
     a.buf_len = buf_len;
     a.stop = range_len;
     a.entry = entry;
+    a.d_entry = d_entry;
     a.gofs = global_offset;
     a.spec = d_spec;
     a.spec_n = d_spec_n;

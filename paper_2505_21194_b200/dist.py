@@ -83,17 +83,58 @@ def _allgather_i64(values, group, device):
     return torch.stack(out).cpu().tolist()
 
 
+def _allgather_dev(t, group):
+    """all_gather of a small device tensor, stream-ordered (no host sync)."""
+    P = dist.get_world_size(group)
+    out = torch.empty((P,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    else:
+        dist.all_gather(list(out.unbind(0)), t.contiguous(), group=group)
+    return out
+
+
 def chunk_sharded(shard: Shard, backend, group=None, comm_device=None) -> ShardResult:
-    """Run the sharded protocol for this rank (collective: every rank calls it)."""
+    """Run the sharded protocol for this rank (collective: every rank calls it).
+    Backends with a device path (the CUDA one, exchanging over NCCL) enqueue the
+    speculative pass, both exchanges and the re-synchronisation without a host
+    sync and check once at the end (`_device_round`); the host loop below
+    handles everything else, including further rounds when an overhang changed."""
     P = dist.get_world_size(group)
     r = dist.get_rank(group)
     dev = comm_device if comm_device is not None else backend.comm_device
     if P > 1 and r < P - 1 and shard.range_len < backend.max_size:
         raise ValueError("a non-final range must hold at least max_size bytes")
+    if getattr(backend, "device_protocol", False) and getattr(dev, "type", str(dev)) != "cpu":
+        done = _device_round(shard, backend, group, P, r)
+        if done is not None:
+            return done
     spec = backend.spec(shard)
     info = _allgather_i64([spec.overhang, spec.count], group, dev)
-    cur, cur_entry = spec, shard.global_offset
-    rounds, rewalked = 0, 0
+    return _host_rounds(shard, backend, group, dev, P, r, spec, info, spec, shard.global_offset, 0, 0)
+
+
+def _device_round(shard, backend, group, P, r):
+    """One speculative pass + one exchange + one re-synchronisation, all on the
+    stream; a single host read at the end decides whether it was final (the
+    usual case) -- else None and the caller runs the host loop from scratch."""
+    spec = backend.spec_dev(shard)                      # Chain; extra["sum"] = device [overhang, count]
+    info = _allgather_dev(spec.extra["sum"], group)     # [P, 2]
+    if r > 0:
+        cur = backend.resync_dev(shard, info[r - 1, 0:1], spec)
+    else:
+        cur = spec
+    info2 = _allgather_dev(cur.extra["sum"], group)     # [P, 2]
+    h = torch.cat([info.reshape(-1), info2.reshape(-1)]).cpu().tolist()
+    a, b = h[:2 * P], h[2 * P:]
+    if any(a[2 * k] != b[2 * k] for k in range(P)):      # an overhang changed: more rounds needed
+        return None
+    counts = [b[2 * k + 1] for k in range(P)]
+    entry = a[2 * (r - 1)] if r > 0 else shard.global_offset
+    return ShardResult(cur.cuts, counts[r], sum(counts[:r]), sum(counts), 1, cur.extra.get("rewalked", 0), entry)
+
+
+def _host_rounds(shard, backend, group, dev, P, r, spec, info, cur, cur_entry, rounds, rewalked):
     while True:
         true_entry = info[r - 1][0] if r > 0 else shard.global_offset
         changed = 0
@@ -124,6 +165,7 @@ class CudaRangeBackend:
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.comm_device = self.device
         self.stream = stream
+        self.device_protocol = True      # spec_dev / resync_dev: no host sync inside a round
         self._key = None
 
     def _alloc(self, shard: Shard):
@@ -172,3 +214,30 @@ class CudaRangeBackend:
         if k == 0:
             last = shard.global_offset + entry
         return Chain(self.out_cuts, k, last, {"merged": bool(st[0]), "rewalked": int(st[1])})
+
+    # ---- device path: summaries stay on the GPU (for NCCL all_gather), no host sync
+    def _summary(self, cuts, ncuts, empty_overhang: int):
+        k = ncuts.reshape(1)
+        last = cuts.gather(0, (k - 1).clamp_min(0))
+        ov = torch.where(k > 0, last, torch.full_like(last, empty_overhang))
+        return torch.cat([ov, k])
+
+    def spec_dev(self, shard: Shard) -> Chain:
+        from . import range_chunk_into
+        self._alloc(shard)
+        with torch.cuda.device(self.device):
+            range_chunk_into(shard.buf, shard.range_len, 0, shard.global_offset, self.p, self.spec_cuts, self.spec_n,
+                             workspace=self.ws, stream=self.stream)
+            sm = self._summary(self.spec_cuts, self.spec_n, shard.global_offset)
+        return Chain(self.spec_cuts, -1, -1, {"sum": sm})
+
+    def resync_dev(self, shard: Shard, d_entry, spec: Chain) -> Chain:
+        """d_entry: int64 CUDA tensor [1] holding the true entry as a global offset."""
+        from . import range_resync_dev_into
+        self._alloc(shard)
+        with torch.cuda.device(self.device):
+            e = d_entry.contiguous()
+            range_resync_dev_into(shard.buf, shard.range_len, e, shard.global_offset, self.p, spec.cuts,
+                                  self.spec_n, self.out_cuts, self.out_n, self.status, stream=self.stream)
+            sm = torch.cat([self.status[3:4], self.out_n.reshape(1)])
+        return Chain(self.out_cuts, -1, -1, {"sum": sm})

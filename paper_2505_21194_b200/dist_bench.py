@@ -32,7 +32,7 @@ def run(args, metric, workload, cfg):
         cdev = dev
     else:
         dist.init_process_group(backend)
-        cdev = torch.device("cpu")
+        cdev = dev                      # gloo handles CUDA tensors too: same device protocol as NCCL
     try:
         n_per = args.bytes_per_gpu
         n = n_per * world

@@ -92,7 +92,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, P, port, kind, seed, n, pidx, q):
+def _worker(rank, P, port, kind, seed, n, pidx, q, comm="cpu"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=P)
@@ -107,8 +107,9 @@ def _worker(rank, P, port, kind, seed, n, pidx, q):
         else:
             synth.fill_device(kind, seed, lo, buf)
         be = CudaRangeBackend(p)
-        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=torch.device("cpu"))
-        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=torch.device("cpu"))   # buffers reused
+        cd = torch.device(comm)
+        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=cd)
+        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=cd)   # buffers reused
         cuts = res.cuts[: res.count].cpu().numpy().tolist()
         allc = [None] * P
         dist.all_gather_object(allc, (rank, res.first_index, res.total, res.rounds, cuts))
@@ -121,14 +122,21 @@ def _worker(rank, P, port, kind, seed, n, pidx, q):
 SHARD_PARAMS = [oracle.table1(8), oracle.table1(4, 1), oracle.table1(16)]
 
 
-@pytest.mark.parametrize("P,kind,seed,n,pidx", [(2, "rampmix", 41, 24 << 20, 0), (3, "markov", 42, 20 << 20, 1),
-                                                 (4, "uniform", 43, 30 << 20, 2), (3, "zeros", 0, 5 << 20, 0)])
-def test_sharded_protocol_on_one_gpu(P, kind, seed, n, pidx):
+@pytest.mark.parametrize("P,kind,seed,n,pidx,comm", [(2, "rampmix", 41, 24 << 20, 0, "cpu"),
+                                                      (3, "markov", 42, 20 << 20, 1, "cpu"),
+                                                      (4, "uniform", 43, 30 << 20, 2, "cpu"),
+                                                      (3, "zeros", 0, 5 << 20, 0, "cpu"),
+                                                      (3, "markov", 44, 20 << 20, 1, "cuda"),
+                                                      (4, "zeros", 0, 5 << 20, 0, "cuda")])
+def test_sharded_protocol_on_one_gpu(P, kind, seed, n, pidx, comm):
+    """comm="cuda": the device protocol (no host sync inside the round; the
+    exchanges run on device tensors), falling back to the host loop on the
+    phase-locked stream."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, P, port, kind, seed, n, pidx, q)) for r in range(P)]
+    procs = [ctx.Process(target=_worker, args=(r, P, port, kind, seed, n, pidx, q, comm)) for r in range(P)]
     for pr in procs:
         pr.start()
     allc = q.get(timeout=600)
