@@ -31,6 +31,7 @@ EXPORTS = (
     "seqcdc_workspace_size", "seqcdc_chunk", "seqcdc_chunk_batch", "seqcdc_strerror",
     "seqcdc_build_info", "seqcdc_set_segment_bytes", "seqcdc_profile_enable", "seqcdc_profile_collect",
     "seqcdc_range_max_cuts", "seqcdc_range_chunk", "seqcdc_range_resync", "seqcdc_range_resync_dev",
+    "seqcdc_range_chunk_tail", "seqcdc_range_merge_tail",
     "seqcdc_fingerprint", "seqcdc_dedup_workspace_size", "seqcdc_dedup",
 )
 
@@ -116,6 +117,10 @@ def lib():
         L.seqcdc_range_resync.restype = ctypes.c_int
         L.seqcdc_range_resync_dev.argtypes = [p, u64, u64, p, u64, P, p, p, p, p, p, p]
         L.seqcdc_range_resync_dev.restype = ctypes.c_int
+        L.seqcdc_range_chunk_tail.argtypes = [p, u64, u64, u64, u64, P, p, p, u32, p, p, p, sz, p]
+        L.seqcdc_range_chunk_tail.restype = ctypes.c_int
+        L.seqcdc_range_merge_tail.argtypes = [p, u64, u64, u64, P, p, u32, p, p, p, p, p, p]
+        L.seqcdc_range_merge_tail.restype = ctypes.c_int
         L.seqcdc_fingerprint.argtypes = [p, p, p, u64, p, p]
         L.seqcdc_fingerprint.restype = ctypes.c_int
         L.seqcdc_dedup_workspace_size.argtypes = [u64]
@@ -324,3 +329,32 @@ def range_resync_dev_into(buf, range_len: int, d_entry, global_offset: int, p: S
                                        cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(),
                                        status.data_ptr(), _stream_ptr(stream, buf.device))
     _check(rc, "seqcdc_range_resync_dev")
+
+
+def range_chunk_tail_into(buf, range_len: int, global_offset: int, p: SeqParams, cuts, ncuts, tail_max: int,
+                          tail, tail_n, workspace=None, stream=None) -> None:
+    """Asynchronous seqcdc_range_chunk_tail (entry 0): the speculative chain of the
+    range plus up to ``tail_max`` cuts past its overhang into ``tail``/``tail_n``."""
+    _require_cuda(buf, "buf")
+    cp = p.c()
+    ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    rc = lib().seqcdc_range_chunk_tail(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len, 0,
+                                       global_offset, ctypes.byref(cp), cuts.data_ptr() if cuts.numel() else None,
+                                       ncuts.data_ptr(), tail_max, tail.data_ptr() if tail_max else None,
+                                       tail_n.data_ptr() if tail_max else None, ws_ptr, ws_len,
+                                       _stream_ptr(stream, buf.device))
+    _check(rc, "seqcdc_range_chunk_tail")
+
+
+def range_merge_tail_into(buf, range_len: int, global_offset: int, p: SeqParams, prev_block, tail_max: int, spec,
+                          spec_n, cuts, ncuts, status, stream=None) -> None:
+    """Asynchronous seqcdc_range_merge_tail: ``prev_block`` = int64 CUDA
+    [2 + tail_max] = (tail_n, overhang, tail...) of the previous range."""
+    _require_cuda(buf, "buf")
+    cp = p.c()
+    rc = lib().seqcdc_range_merge_tail(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len,
+                                       global_offset, ctypes.byref(cp), prev_block.data_ptr(), tail_max,
+                                       spec.data_ptr() if spec.numel() else None, spec_n.data_ptr(),
+                                       cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(),
+                                       status.data_ptr(), _stream_ptr(stream, buf.device))
+    _check(rc, "seqcdc_range_merge_tail")

@@ -89,6 +89,11 @@ struct Work {
     uint32_t *ctrl;
     // outputs
     uint64_t *cuts, *cut_index, *ncuts;
+    // range calls: the chain continued past its overhang for up to tail_max cuts
+    // (only chunks wholly inside the buffer), for the next rank's local merge
+    uint64_t *tail;        // [tail_max] global offsets: tail[0] = the overhang
+    uint64_t *tail_n;      // count written (0 = none / invalid)
+    uint32_t tail_max;
 };
 
 struct Seg {
@@ -380,6 +385,21 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
     publish(w.Lcnt + s, lb.n, true, lane);
     TL_MARK(s, 1);
     if (!extend) {                       // the stream's last segment: no extension
+        if (w.single && w.tail_max) {    // range call: continue past the overhang (next rank's merge)
+            ListBuf tb{0, 0};
+            if (c >= stop_rel && c < end_rel) {
+                lb_push(tb, off + c + w.out_add, w.tail, lane);
+                base = c;
+#pragma unroll 1
+                while (tb.n < w.tail_max && base + w.p.mx <= end_rel) {
+                    c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+                    lb_push(tb, off + c + w.out_add, w.tail, lane);
+                    base = c;
+                }
+            }
+            lb_flush(tb, w.tail, lane);
+            if (lane == 0) *w.tail_n = tb.n;
+        }
         if (lane == 0) {
             w.Xcnt[s] = 0;
             w.target[s] = TGT_END;
@@ -801,6 +821,7 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
     const uint64_t last = cnt[k - 1];
     smem_scan_excl(cnt, k);
     if (blockIdx.x == 0 && tid == 0) {
+        if (w.tail_n && en[k - 1] == ENTRY_DEAD) *w.tail_n = 0;   // its chain is not the valid one
         const uint64_t total = cnt[k - 1] + last;
         w.cut_index[0] = 0;
         w.cut_index[1] = total;
@@ -924,7 +945,7 @@ static int device_info(int &sms, int &occ, uint32_t smem = 0)
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int sms, int occ, Plan &pl,
-                      bool single, uint64_t stop)
+                      bool single, uint64_t stop, bool short_tail = false)
 {
     // up to ~1.5 GiB the run ends with the longest seam extension, and 22 walkers
     // per SM (longer segments, less contention on the tail) measured ~4% faster
@@ -942,6 +963,15 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     if (g_force_G) G = std::max<uint64_t>(g_force_G, mx);
     G = std::min<uint64_t>(G, std::max<uint64_t>(G_CEIL, mx));
     G = (G + mx - 1) / mx * mx;
+    if (single && short_tail) {
+        // range call with a tail: the last segment's walker also continues the
+        // chain past the range end (~96 chunks), so give it a third of a segment
+        const uint64_t ns1 = stop <= G ? 1 : (stop + G - 1) / G;
+        if (ns1 >= 3) {
+            const uint64_t Gt = (stop - G / 3 + (ns1 - 1) - 1) / (ns1 - 1);
+            if (Gt * (ns1 - 1) < stop && Gt >= mx) G = Gt;
+        }
+    }
     pl.G = G;
     if (single) {
         pl.nseg1 = (uint32_t)(stop <= G ? 1 : (stop + G - 1) / G);
@@ -1052,6 +1082,11 @@ static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, 
     k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
 }
 
+struct TailReq {
+    uint64_t *tail = nullptr, *tail_n = nullptr;
+    uint32_t max = 0;
+};
+
 template <int MODE>
 static void launch_ms(int ms, const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
 {
@@ -1063,7 +1098,7 @@ static void launch_ms(int ms, const Work &w, const Plan &pl, int sms, cudaStream
 static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total, uint64_t stop,
                uint64_t out_add, const seqcdc_params_t *p, const DevParams &geo, uint64_t *d_cuts, uint64_t *d_cut_index,
                uint64_t *d_ncuts, uint8_t *ws, size_t ws_bytes, const Plan &pl, int sms, cudaStream_t st,
-               bool single)
+               bool single, const TailReq &tail)
 {
     if (ws_bytes < pl.bytes) return SEQCDC_ENOMEM;
     if (total / pl.G + 2 > STITCH_MAX_SEGS) return SEQCDC_EINVAL;  // one stream's segments fit the stitch smem
@@ -1113,6 +1148,10 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.cuts = d_cuts;
     w.cut_index = d_cut_index;
     w.ncuts = d_ncuts;
+    w.tail = tail.tail;
+    w.tail_n = tail.tail_n;
+    w.tail_max = tail.max;
+    if (tail.max && cudaMemsetAsync(tail.tail_n, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
 
     ProfRec rec, *pr = nullptr;
     {
@@ -1150,7 +1189,8 @@ constexpr size_t SINGLE_EXTRA = 256;
 
 static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total, uint64_t stop,
                    uint64_t out_add, const seqcdc_params_t *p, uint64_t *d_cuts, uint64_t *d_cut_index,
-                   uint64_t *d_ncuts, void *d_ws, size_t ws_bytes, cudaStream_t st, bool single_api)
+                   uint64_t *d_ncuts, void *d_ws, size_t ws_bytes, cudaStream_t st, bool single_api,
+                   const TailReq &tail = TailReq())
 {
     DevParams geo;
     ring_geometry(p, geo);
@@ -1159,7 +1199,7 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
     if (rc) return rc;
     g_last_occ = occ;
     Plan pl;
-    make_plan(total, ns, p, sms, occ, pl, single_api, stop);
+    make_plan(total, ns, p, sms, occ, pl, single_api, stop, tail.max > 0);
     const size_t extra = single_api ? SINGLE_EXTRA : 0;
     uint8_t *ws = (uint8_t *)d_ws;
     bool owned = false;
@@ -1177,7 +1217,7 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
         d_cut_index = offs + 2;
     }
     rc = run(d_in, d_offsets, ns, total, stop, out_add, p, geo, d_cuts, d_cut_index, d_ncuts, ws + extra, pl.bytes,
-             pl, sms, st, single_api);
+             pl, sms, st, single_api, tail);
     if (owned) cudaFreeAsync(ws, st);
     return rc;
 }
@@ -1251,9 +1291,11 @@ SEQCDC_API size_t seqcdc_workspace_size(uint64_t total, uint32_t ns, const seqcd
     }
     Plan pl;
     Plan pb;
+    Plan pt;
     make_plan(total, ns ? ns : 1, p, sms, occ, pl, ns <= 1, total);
     make_plan(total, ns ? ns : 1, p, sms, occ, pb, false, total);
-    return std::max(pl.bytes, pb.bytes) + SINGLE_EXTRA;
+    make_plan(total, 1, p, sms, occ, pt, true, total, true);
+    return std::max(std::max(pl.bytes, pb.bytes), pt.bytes) + SINGLE_EXTRA;
 }
 
 SEQCDC_API int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total,
@@ -1287,6 +1329,29 @@ SEQCDC_API uint64_t seqcdc_range_max_cuts(uint64_t buf_len, uint64_t range_len, 
     if (!p || !p->min_size) return 0;
     const uint64_t span = std::min<uint64_t>(buf_len, range_len + p->max_size);
     return span / p->min_size + 2;
+}
+
+SEQCDC_API int seqcdc_range_chunk_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                                       uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
+                                       uint64_t *d_ncuts, uint32_t tail_max, uint64_t *d_tail, uint64_t *d_tail_n,
+                                       void *d_ws, size_t ws_bytes, void *stream)
+{
+    if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
+    if (!d_ncuts || range_len > buf_len || entry > range_len) return SEQCDC_EINVAL;
+    if (tail_max && (!d_tail || !d_tail_n)) return SEQCDC_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (entry >= range_len) {
+        if (cudaMemsetAsync(d_ncuts, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
+        if (tail_max && cudaMemsetAsync(d_tail_n, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
+        return SEQCDC_OK;
+    }
+    if (!d_buf || !d_cuts) return SEQCDC_EINVAL;
+    TailReq t;
+    t.tail = d_tail;
+    t.tail_n = d_tail_n;
+    t.max = tail_max;
+    return enqueue(d_buf + entry, nullptr, 1, buf_len - entry, range_len - entry, global_offset + entry, p, d_cuts,
+                   nullptr, d_ncuts, d_ws, ws_bytes, st, true, t);
 }
 
 SEQCDC_API int seqcdc_range_chunk(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,

@@ -34,6 +34,7 @@ struct ResyncArgs {
     const uint8_t *buf;
     uint64_t buf_len, stop, entry, gofs;
     const uint64_t *d_entry;  // if set: the entry as a GLOBAL offset, read on the device
+    const uint64_t *skip;     // if set and *skip != 0: a merge already settled the result
     const uint64_t *spec;     // speculative cut list (global offsets, ascending)
     const uint64_t *spec_n;   // its length (device)
     uint64_t *out, *ncuts, *status;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(32) k_resync(ResyncArgs a)
 {
     __shared__ __align__(128) uint8_t ring[RING];
     const int lane = threadIdx.x;
+    if (a.skip && *a.skip != 0) return;
     Walker wk;
     walker_init(wk, ring, a.p, lane);
     const uint64_t abase = (uint64_t)(uintptr_t)a.buf;
@@ -146,6 +148,55 @@ __global__ void __launch_bounds__(256) k_resync_tail(ResyncArgs a)
     }
 }
 
+// Rank r's local merge with rank r-1's tail: blk = [n, overhang, e_0 .. e_{n-1}],
+// the true chain from rank r's entry (e_0 = the overhang).  The first e_i that
+// is also a speculative cut of this range is a merge: the result is e_1..e_i
+// followed by the speculative cuts after it (k_resync_tail).  No merge within
+// the tail (or no tail) leaves status merged = 0 for the re-walk fallback.
+__global__ void __launch_bounds__(128) k_merge_tail(const uint64_t *blk, uint32_t tail_max, ResyncArgs a)
+{
+    __shared__ unsigned long long best;                  // (i << 32) | j of the first merge
+    const uint64_t n = min(blk[0], (uint64_t)tail_max);
+    const uint64_t *e = blk + 2;
+    const uint64_t k = *a.spec_n;
+    const uint64_t ov = blk[1];
+    if (threadIdx.x == 0) best = ~0ull;
+    __syncthreads();
+    if (ov >= a.gofs + a.stop) {                         // no chunk starts in this range
+        if (threadIdx.x == 0) {
+            *a.ncuts = 0;
+            a.status[ST_MERGED] = 2;
+            a.status[ST_M] = 0;
+            a.status[ST_J] = 0;
+            a.status[ST_OVERHANG] = ov;
+        }
+        return;
+    }
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t x = e[i];
+        uint64_t lo = 0, hi = k;                         // binary search in the ascending spec list
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (__ldcg(a.spec + mid) < x) lo = mid + 1; else hi = mid;
+        }
+        if (lo < k && __ldcg(a.spec + lo) == x) atomicMin(&best, ((unsigned long long)i << 32) | lo);
+    }
+    __syncthreads();
+    const unsigned long long b = best;
+    if (b == ~0ull) {
+        if (threadIdx.x == 0) a.status[ST_MERGED] = 0;   // fallback: re-walk from the overhang
+        return;
+    }
+    const uint64_t im = b >> 32, jm = b & 0xffffffffull;
+    for (uint64_t t = threadIdx.x; t < im; t += blockDim.x) a.out[t] = e[t + 1];
+    if (threadIdx.x == 0) {
+        a.status[ST_MERGED] = 1;
+        a.status[ST_M] = im;
+        a.status[ST_J] = jm;
+        a.status[ST_OVERHANG] = ov;
+    }
+}
+
 __global__ void k_resync_empty(uint64_t *ncuts, uint64_t *status, uint64_t overhang)
 {
     *ncuts = 0;
@@ -178,7 +229,18 @@ using namespace seqcdc;
 static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
                        const uint64_t *d_entry, uint64_t global_offset, const seqcdc_params_t *p,
                        const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
-                       uint64_t *d_status, void *stream);
+                       uint64_t *d_status, void *stream, const uint64_t *merge_blk = nullptr,
+                       uint32_t tail_max = 0);
+
+SEQCDC_API int seqcdc_range_merge_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
+                                       uint64_t global_offset, const seqcdc_params_t *p, const uint64_t *d_prev,
+                                       uint32_t tail_max, const uint64_t *d_spec, const uint64_t *d_spec_n,
+                                       uint64_t *d_cuts, uint64_t *d_ncuts, uint64_t *d_status, void *stream)
+{
+    if (!d_prev) return SEQCDC_EINVAL;
+    return resync_impl(d_buf, buf_len, range_len, 0, d_prev + 1, global_offset, p, d_spec, d_spec_n, d_cuts, d_ncuts,
+                       d_status, stream, d_prev, tail_max);
+}
 
 SEQCDC_API int seqcdc_range_resync_dev(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
                                        const uint64_t *d_entry, uint64_t global_offset, const seqcdc_params_t *p,
@@ -202,7 +264,7 @@ SEQCDC_API int seqcdc_range_resync(const uint8_t *d_buf, uint64_t buf_len, uint6
 static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
                        const uint64_t *d_entry, uint64_t global_offset, const seqcdc_params_t *p,
                        const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
-                       uint64_t *d_status, void *stream)
+                       uint64_t *d_status, void *stream, const uint64_t *merge_blk, uint32_t tail_max)
 {
     if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
     if (!d_ncuts || !d_status || !d_spec_n || range_len > buf_len || entry > range_len) return SEQCDC_EINVAL;
@@ -233,6 +295,10 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
     a.p.mx = (uint32_t)p->max_size;
     a.p.mnL = (uint32_t)p->min_size - p->seq_length;
     seqcdc_ring_geometry(p, &a.p.bs, &a.p.nb, &a.p.ah);
+    if (merge_blk) {              // local merge first; the re-walk runs only if it found none
+        k_merge_tail<<<1, 128, 0, st>>>(merge_blk, tail_max, a);
+        a.skip = d_status;
+    }
     const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
     switch (p->mode | ((p->flags & SEQCDC_FLAG_SIGNED) ? 2u : 0u)) {
     case 0: launch_ms<0>(ms, a, st); break;

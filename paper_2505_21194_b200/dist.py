@@ -115,23 +115,27 @@ def chunk_sharded(shard: Shard, backend, group=None, comm_device=None) -> ShardR
 
 
 def _device_round(shard, backend, group, P, r):
-    """One speculative pass + one exchange + one re-synchronisation, all on the
-    stream; a single host read at the end decides whether it was final (the
-    usual case) -- else None and the caller runs the host loop from scratch."""
-    spec = backend.spec_dev(shard)                      # Chain; extra["sum"] = device [overhang, count]
-    info = _allgather_dev(spec.extra["sum"], group)     # [P, 2]
-    if r > 0:
-        cur = backend.resync_dev(shard, info[r - 1, 0:1], spec)
-    else:
-        cur = spec
-    info2 = _allgather_dev(cur.extra["sum"], group)     # [P, 2]
-    h = torch.cat([info.reshape(-1), info2.reshape(-1)]).cpu().tolist()
-    a, b = h[:2 * P], h[2 * P:]
-    if any(a[2 * k] != b[2 * k] for k in range(P)):      # an overhang changed: more rounds needed
+    """One exchange round, all enqueued on the stream; a single host read at the
+    end decides whether it was final (the usual case) -- else None and the
+    caller runs the host loop from scratch.
+
+    Each rank's speculative pass also continues its chain ~96 cuts past its
+    overhang (``tail``); one all_gather of (tail_n, overhang, tail) blocks lets
+    rank r find where the true chain entering its range meets its own
+    speculative chain -- a local search, no walking (seqcdc_range_merge_tail;
+    a re-walk only if the tail is too short).  A second all_gather of
+    (overhang, count, speculative overhang) gives the global prefix and proves
+    no overhang changed."""
+    spec = backend.spec_dev_tail(shard, last=(r == P - 1))   # extra: "block" [2 + E], "sum" [2]
+    blocks = _allgather_dev(spec.extra["block"], group)     # [P, 2 + E]
+    cur = backend.merge_dev(shard, blocks[r - 1], spec) if r > 0 else spec
+    info = _allgather_dev(torch.cat([cur.extra["sum"], spec.extra["sum"][0:1]]), group)   # [P, 3]
+    h = info.reshape(-1).cpu().tolist()
+    if any(h[3 * k] != h[3 * k + 2] for k in range(P)):     # an overhang changed: more rounds needed
         return None
-    counts = [b[2 * k + 1] for k in range(P)]
-    entry = a[2 * (r - 1)] if r > 0 else shard.global_offset
-    return ShardResult(cur.cuts, counts[r], sum(counts[:r]), sum(counts), 1, cur.extra.get("rewalked", 0), entry)
+    counts = [h[3 * k + 1] for k in range(P)]
+    entry = h[3 * (r - 1)] if r > 0 else shard.global_offset
+    return ShardResult(cur.cuts, counts[r], sum(counts[:r]), sum(counts), 1, 0, entry)
 
 
 def _host_rounds(shard, backend, group, dev, P, r, spec, info, cur, cur_entry, rounds, rewalked):
@@ -158,6 +162,8 @@ class CudaRangeBackend:
     """The product backend: the C-ABI range calls on the rank's GPU.  Buffers
     are allocated once per shard size and reused across calls."""
 
+    TAIL = 96          # cuts each range continues past its overhang (device protocol)
+
     def __init__(self, params, device=None, stream=None):
         from . import SeqParams  # noqa: F401  (type of params)
         self.p = params
@@ -183,6 +189,7 @@ class CudaRangeBackend:
         self.status = torch.zeros(4, dtype=torch.int64, device=dev)
         self.ws = torch.empty(workspace_size(n, 1, self.p), dtype=torch.uint8, device=dev)
         self.host = torch.empty(8, dtype=torch.int64, pin_memory=True)
+        self.block = torch.zeros(2 + self.TAIL, dtype=torch.int64, device=dev)
         self._key = key
 
     def _read(self, cuts, ncuts, extra=None) -> list[int]:
@@ -238,6 +245,30 @@ class CudaRangeBackend:
         with torch.cuda.device(self.device):
             e = d_entry.contiguous()
             range_resync_dev_into(shard.buf, shard.range_len, e, shard.global_offset, self.p, spec.cuts,
+                                  self.spec_n, self.out_cuts, self.out_n, self.status, stream=self.stream)
+            sm = torch.cat([self.status[3:4], self.out_n.reshape(1)])
+        return Chain(self.out_cuts, -1, -1, {"sum": sm})
+
+    # ---- one-exchange device protocol (tails)
+    def spec_dev_tail(self, shard: Shard, last: bool) -> Chain:
+        from . import range_chunk_tail_into
+        self._alloc(shard)
+        E = 0 if last else self.TAIL
+        with torch.cuda.device(self.device):
+            self.block[0].zero_()
+            range_chunk_tail_into(shard.buf, shard.range_len, shard.global_offset, self.p, self.spec_cuts,
+                                  self.spec_n, E, self.block[2:], self.block[0:1], workspace=self.ws,
+                                  stream=self.stream)
+            sm = self._summary(self.spec_cuts, self.spec_n, shard.global_offset)
+            self.block[1:2].copy_(sm[0:1])
+        return Chain(self.spec_cuts, -1, -1, {"sum": sm, "block": self.block})
+
+    def merge_dev(self, shard: Shard, prev_block, spec: Chain) -> Chain:
+        from . import range_merge_tail_into
+        self._alloc(shard)
+        with torch.cuda.device(self.device):
+            pb = prev_block.contiguous()
+            range_merge_tail_into(shard.buf, shard.range_len, shard.global_offset, self.p, pb, self.TAIL, spec.cuts,
                                   self.spec_n, self.out_cuts, self.out_n, self.status, stream=self.stream)
             sm = torch.cat([self.status[3:4], self.out_n.reshape(1)])
         return Chain(self.out_cuts, -1, -1, {"sum": sm})

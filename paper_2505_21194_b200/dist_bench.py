@@ -38,7 +38,8 @@ def run(args, metric, workload, cfg):
         n = n_per * world
         p = sc.SeqParams.table1(cfg["avg_kib"], cfg["mode"])
         lo, hi = rank * n_per, (rank + 1) * n_per
-        end = n if rank == world - 1 else min(n, hi + p.max_size)
+        # halo: room for the range's tail continuation (device protocol, dist.py)
+        end = n if rank == world - 1 else min(n, hi + (CudaRangeBackend.TAIL + 1) * p.max_size)
         buf = torch.empty(end - lo, dtype=torch.uint8, device=dev)
         synth.fill_device(cfg["kind"], cfg["seed"], lo, buf)
         shard = Shard(buf, hi - lo, lo)

@@ -100,7 +100,7 @@ def _worker(rank, P, port, kind, seed, n, pidx, q, comm="cpu"):
         from paper_2505_21194_b200.dist import CudaRangeBackend, Shard, chunk_sharded
         p = _sp(SHARD_PARAMS[pidx])
         lo, hi = n * rank // P, n * (rank + 1) // P
-        end = n if rank == P - 1 else min(n, hi + p.max_size)
+        end = n if rank == P - 1 else min(n, hi + (CudaRangeBackend.TAIL + 1) * p.max_size)
         buf = torch.empty(end - lo, dtype=torch.uint8, device="cuda")
         if kind == "zeros":
             buf.zero_()
@@ -151,3 +151,51 @@ def test_sharded_protocol_on_one_gpu(P, kind, seed, n, pidx, comm):
         got += cuts
         assert total == want.size
     assert np.array_equal(np.asarray(got, np.uint64), want)
+
+
+@pytest.mark.parametrize("kind,seed,p", CASES)
+def test_range_tail_and_local_merge(kind, seed, p):
+    """seqcdc_range_chunk_tail's tail = the oracle chain continued past the
+    overhang (fully determined chunks only); seqcdc_range_merge_tail on the next
+    range = the true chain of that range, whether the tail reaches the merge or
+    the re-walk fallback runs (tiny tail_max)."""
+    n = 8 << 20
+    b = synth.fill_host(kind, seed, 0, n)
+    sp = _sp(p)
+    R = [0, 3 << 20, n]
+    E = 96
+    full = oracle.chunk(b, p)
+    for tail_max in (E, 2):
+        # range 0 with its halo
+        end0 = min(n, R[1] + (E + 1) * p.max_size)
+        buf0 = torch.from_numpy(b[:end0]).cuda()
+        cap0 = sc.range_max_cuts(buf0.numel(), R[1], sp)
+        c0 = torch.empty(cap0, dtype=torch.int64, device="cuda")
+        n0 = torch.zeros(1, dtype=torch.int64, device="cuda")
+        blk = torch.zeros(2 + E, dtype=torch.int64, device="cuda")
+        sc.range_chunk_tail_into(buf0, R[1], 0, sp, c0, n0, tail_max, blk[2:], blk[0:1])
+        k0 = int(n0.item())
+        ov = int(c0[k0 - 1].item())
+        blk[1] = ov
+        tn = int(blk[0].item())
+        tail = blk[2:2 + tn].cpu().numpy().astype(np.uint64)
+        # oracle: the true chain from the overhang, chunks wholly inside the buffer
+        want_tail = [ov]
+        base = ov
+        while len(want_tail) < tail_max and base + p.max_size <= end0:
+            base = oracle.next_cut(b[:end0], base, p)
+            want_tail.append(base)
+        assert tail.tolist() == want_tail, (kind, tail_max)
+        # range 1: speculative pass + local merge with range 0's tail
+        buf1 = torch.from_numpy(b[R[1]:]).cuda()
+        cap1 = sc.range_max_cuts(buf1.numel(), R[2] - R[1], sp)
+        spec = torch.empty(cap1, dtype=torch.int64, device="cuda")
+        spec_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+        sc.range_chunk_into(buf1, R[2] - R[1], 0, R[1], sp, spec, spec_n)
+        out = torch.empty(cap1, dtype=torch.int64, device="cuda")
+        out_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+        status = torch.zeros(4, dtype=torch.int64, device="cuda")
+        sc.range_merge_tail_into(buf1, R[2] - R[1], R[1], sp, blk, E if tail_max == E else tail_max, spec, spec_n,
+                                 out, out_n, status)
+        got = out[: int(out_n.item())].cpu().numpy().astype(np.uint64)
+        assert np.array_equal(got, full[full > ov]), (kind, tail_max, status.cpu().tolist())
