@@ -227,32 +227,39 @@ int seqcdc_dedup(const uint8_t *d_digests, const uint64_t *d_cuts, const uint64_
 /*
  * One-exchange sharding (dist.py's device protocol).
  *
- * seqcdc_range_chunk_tail: seqcdc_range_chunk that also continues the range's
- * chain past its overhang for up to tail_max cuts, stopping before any chunk
- * that would reach past buf_len (so only fully determined chunks are
- * written): d_tail[0] = the overhang, d_tail[1..] the next cuts (global
- * offsets), *d_tail_n = their number (0 when the range's valid chain does not
- * come from its last segment -- the next range then re-walks instead).  The
- * halo must hold those chunks (about tail_max * max_size bytes).  The range's
- * last segment is shortened so this extra walk stays off the critical path.
+ * A range's exchange block is uint64 [3 + tail_max] = {overhang, number of
+ * cuts, tail_n, tail[0 .. tail_max)}.
+ *
+ * seqcdc_range_chunk_tail: seqcdc_range_chunk that also fills the block:
+ * d_summary[0..2) = {overhang (the range's last cut), number of cuts}
+ * (optional) and the chain continued past the overhang for up to tail_max
+ * cuts, stopping before any chunk that would reach past buf_len (so only
+ * fully determined chunks are written): d_tail[0] = the overhang, d_tail[1..]
+ * the next cuts (global offsets), *d_tail_n = their number (0 when the
+ * range's valid chain does not come from its last segment -- the next range
+ * then re-walks instead).  The halo must hold those chunks (about tail_max *
+ * max_size bytes).  The range's last segment is shortened so this extra walk
+ * stays off the critical path.
  *
  * seqcdc_range_merge_tail: the next range's side.  d_prev = the previous
- * range's block [tail_n, overhang, tail[0 .. tail_max)] (e.g. a row of an
- * NCCL all_gather).  The true chain of this range starts at the overhang; the
- * first tail cut that is also in this range's speculative list d_spec is a
- * merge, and the result (d_cuts, *d_ncuts, d_status as for
- * seqcdc_range_resync) is the tail up to it plus the speculative cuts after
- * it -- no walking.  Without a merge inside the tail, one warp re-walks from
- * the overhang (seqcdc_range_resync_dev), all enqueued, no host sync.
+ * range's block (e.g. a row of an NCCL all_gather).  The true chain of this
+ * range starts at that overhang; the first tail cut that is also in this
+ * range's speculative list d_spec is a merge, and the result (d_cuts,
+ * *d_ncuts, d_status as for seqcdc_range_resync) is the tail up to it plus the
+ * speculative cuts after it -- no walking.  Without a merge inside the tail,
+ * one warp re-walks from the overhang.  d_sum3 (optional) = {final overhang,
+ * number of cuts, *d_spec_ov} for the second exchange.  All enqueued, no host
+ * sync.
  */
 int seqcdc_range_chunk_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
                             uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
                             uint64_t *d_ncuts, uint32_t tail_max, uint64_t *d_tail, uint64_t *d_tail_n,
-                            void *d_workspace, size_t ws_bytes, void *stream);
+                            uint64_t *d_summary, void *d_workspace, size_t ws_bytes, void *stream);
 int seqcdc_range_merge_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t global_offset,
                             const seqcdc_params_t *p, const uint64_t *d_prev, uint32_t tail_max,
                             const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts,
-                            uint64_t *d_ncuts, uint64_t *d_status, void *stream);
+                            uint64_t *d_ncuts, uint64_t *d_status, const uint64_t *d_spec_ov, uint64_t *d_sum3,
+                            void *stream);
 
 /* Testing / tuning knob: force the segment length G (rounded up to a
  * multiple of max_size, and to at least max_size) used to split streams into

@@ -117,9 +117,9 @@ def lib():
         L.seqcdc_range_resync.restype = ctypes.c_int
         L.seqcdc_range_resync_dev.argtypes = [p, u64, u64, p, u64, P, p, p, p, p, p, p]
         L.seqcdc_range_resync_dev.restype = ctypes.c_int
-        L.seqcdc_range_chunk_tail.argtypes = [p, u64, u64, u64, u64, P, p, p, u32, p, p, p, sz, p]
+        L.seqcdc_range_chunk_tail.argtypes = [p, u64, u64, u64, u64, P, p, p, u32, p, p, p, p, sz, p]
         L.seqcdc_range_chunk_tail.restype = ctypes.c_int
-        L.seqcdc_range_merge_tail.argtypes = [p, u64, u64, u64, P, p, u32, p, p, p, p, p, p]
+        L.seqcdc_range_merge_tail.argtypes = [p, u64, u64, u64, P, p, u32, p, p, p, p, p, p, p, p]
         L.seqcdc_range_merge_tail.restype = ctypes.c_int
         L.seqcdc_fingerprint.argtypes = [p, p, p, u64, p, p]
         L.seqcdc_fingerprint.restype = ctypes.c_int
@@ -332,29 +332,33 @@ def range_resync_dev_into(buf, range_len: int, d_entry, global_offset: int, p: S
 
 
 def range_chunk_tail_into(buf, range_len: int, global_offset: int, p: SeqParams, cuts, ncuts, tail_max: int,
-                          tail, tail_n, workspace=None, stream=None) -> None:
+                          block, workspace=None, stream=None) -> None:
     """Asynchronous seqcdc_range_chunk_tail (entry 0): the speculative chain of the
-    range plus up to ``tail_max`` cuts past its overhang into ``tail``/``tail_n``."""
+    range, and its exchange block (int64 CUDA [3 + tail_max] = overhang, count,
+    tail_n, tail)."""
     _require_cuda(buf, "buf")
     cp = p.c()
     ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    b0 = block.data_ptr()
     rc = lib().seqcdc_range_chunk_tail(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len, 0,
                                        global_offset, ctypes.byref(cp), cuts.data_ptr() if cuts.numel() else None,
-                                       ncuts.data_ptr(), tail_max, tail.data_ptr() if tail_max else None,
-                                       tail_n.data_ptr() if tail_max else None, ws_ptr, ws_len,
+                                       ncuts.data_ptr(), tail_max, b0 + 24 if tail_max else None,
+                                       b0 + 16 if tail_max else None, b0, ws_ptr, ws_len,
                                        _stream_ptr(stream, buf.device))
     _check(rc, "seqcdc_range_chunk_tail")
 
 
 def range_merge_tail_into(buf, range_len: int, global_offset: int, p: SeqParams, prev_block, tail_max: int, spec,
-                          spec_n, cuts, ncuts, status, stream=None) -> None:
-    """Asynchronous seqcdc_range_merge_tail: ``prev_block`` = int64 CUDA
-    [2 + tail_max] = (tail_n, overhang, tail...) of the previous range."""
+                          spec_n, cuts, ncuts, status, spec_ov=None, sum3=None, stream=None) -> None:
+    """Asynchronous seqcdc_range_merge_tail: ``prev_block`` = the previous range's
+    exchange block; ``sum3`` (optional int64 CUDA [3]) = final overhang, count,
+    ``spec_ov[0]``."""
     _require_cuda(buf, "buf")
     cp = p.c()
     rc = lib().seqcdc_range_merge_tail(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len,
                                        global_offset, ctypes.byref(cp), prev_block.data_ptr(), tail_max,
                                        spec.data_ptr() if spec.numel() else None, spec_n.data_ptr(),
                                        cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(),
-                                       status.data_ptr(), _stream_ptr(stream, buf.device))
+                                       status.data_ptr(), spec_ov.data_ptr() if spec_ov is not None else None,
+                                       sum3.data_ptr() if sum3 is not None else None, _stream_ptr(stream, buf.device))
     _check(rc, "seqcdc_range_merge_tail")

@@ -94,6 +94,7 @@ struct Work {
     uint64_t *tail;        // [tail_max] global offsets: tail[0] = the overhang
     uint64_t *tail_n;      // count written (0 = none / invalid)
     uint32_t tail_max;
+    uint64_t *summary;     // range calls (optional): [overhang, number of cuts], written by k_post
 };
 
 struct Seg {
@@ -823,6 +824,23 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
     if (blockIdx.x == 0 && tid == 0) {
         if (w.tail_n && en[k - 1] == ENTRY_DEAD) *w.tail_n = 0;   // its chain is not the valid one
         const uint64_t total = cnt[k - 1] + last;
+        if (w.summary) {                        // the overhang = the last valid cut (k_copy is not needed)
+            uint64_t ov = w.out_add;
+            for (int32_t s3 = (int32_t)k - 1; s3 >= 0; s3--) {
+                const int64_t e = en[s3];
+                if (e == ENTRY_DEAD) continue;
+                const uint64_t nc = __ldcg(w.cont_cnt + s3), nx = __ldcg(w.Xcnt + s3);
+                const uint64_t lc = __ldcg(w.Lcnt + s3) & CNT_MASK;
+                const Seg g = get_seg(w, s3);
+                if (nc) ov = __ldcg(cont_slot(w, s3, __ldcg(w.X + g.Xoff + nx - 1)) + nc - 1) + w.out_add;
+                else if (nx) ov = __ldcg(w.X + g.Xoff + nx - 1) + w.out_add;
+                else if (lc > (uint64_t)(e + 1)) ov = __ldcg(w.L + g.Loff + lc - 1) + w.out_add;
+                else continue;
+                break;
+            }
+            w.summary[0] = ov;
+            w.summary[1] = total;
+        }
         w.cut_index[0] = 0;
         w.cut_index[1] = total;
         *w.ncuts = total;
@@ -848,6 +866,12 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
             for (uint64_t i = lane; i < nc; i += 32) out[nl + nx + i] = __ldcg(Cs + i) + add;
         }
     }
+}
+
+__global__ void k_set2(uint64_t *p, uint64_t a, uint64_t b)
+{
+    p[0] = a;
+    p[1] = b;
 }
 
 __global__ void k_empty(uint64_t *cut_index, uint64_t *ncuts)
@@ -1085,6 +1109,7 @@ static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, 
 struct TailReq {
     uint64_t *tail = nullptr, *tail_n = nullptr;
     uint32_t max = 0;
+    uint64_t *summary = nullptr;
 };
 
 template <int MODE>
@@ -1151,6 +1176,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.tail = tail.tail;
     w.tail_n = tail.tail_n;
     w.tail_max = tail.max;
+    w.summary = tail.summary;
     if (tail.max && cudaMemsetAsync(tail.tail_n, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
 
     ProfRec rec, *pr = nullptr;
@@ -1334,7 +1360,7 @@ SEQCDC_API uint64_t seqcdc_range_max_cuts(uint64_t buf_len, uint64_t range_len, 
 SEQCDC_API int seqcdc_range_chunk_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
                                        uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
                                        uint64_t *d_ncuts, uint32_t tail_max, uint64_t *d_tail, uint64_t *d_tail_n,
-                                       void *d_ws, size_t ws_bytes, void *stream)
+                                       uint64_t *d_summary, void *d_ws, size_t ws_bytes, void *stream)
 {
     if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
     if (!d_ncuts || range_len > buf_len || entry > range_len) return SEQCDC_EINVAL;
@@ -1343,13 +1369,15 @@ SEQCDC_API int seqcdc_range_chunk_tail(const uint8_t *d_buf, uint64_t buf_len, u
     if (entry >= range_len) {
         if (cudaMemsetAsync(d_ncuts, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
         if (tail_max && cudaMemsetAsync(d_tail_n, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
-        return SEQCDC_OK;
+        if (d_summary) k_set2<<<1, 1, 0, st>>>(d_summary, global_offset + entry, 0);
+        return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
     }
     if (!d_buf || !d_cuts) return SEQCDC_EINVAL;
     TailReq t;
     t.tail = d_tail;
     t.tail_n = d_tail_n;
     t.max = tail_max;
+    t.summary = d_summary;
     return enqueue(d_buf + entry, nullptr, 1, buf_len - entry, range_len - entry, global_offset + entry, p, d_cuts,
                    nullptr, d_ncuts, d_ws, ws_bytes, st, true, t);
 }

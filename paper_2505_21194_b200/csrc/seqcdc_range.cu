@@ -35,6 +35,8 @@ struct ResyncArgs {
     uint64_t buf_len, stop, entry, gofs;
     const uint64_t *d_entry;  // if set: the entry as a GLOBAL offset, read on the device
     const uint64_t *skip;     // if set and *skip != 0: a merge already settled the result
+    uint64_t *sum3;           // optional: [final overhang, number of cuts, *spec_ov] (k_resync_tail)
+    const uint64_t *spec_ov;
     const uint64_t *spec;     // speculative cut list (global offsets, ascending)
     const uint64_t *spec_n;   // its length (device)
     uint64_t *out, *ncuts, *status;
@@ -135,7 +137,14 @@ __global__ void __launch_bounds__(32) k_resync(ResyncArgs a)
 __global__ void __launch_bounds__(256) k_resync_tail(ResyncArgs a)
 {
     const uint64_t merged = a.status[ST_MERGED], m = a.status[ST_M];
-    if (merged == 2) return;                          // empty range (written by k_resync)
+    if (merged == 2) {                                // empty range (written by k_resync / k_merge_tail)
+        if (a.sum3 && blockIdx.x == 0 && threadIdx.x == 0) {
+            a.sum3[0] = a.status[ST_OVERHANG];
+            a.sum3[1] = 0;
+            a.sum3[2] = *a.spec_ov;
+        }
+        return;
+    }
     const uint64_t k = *a.spec_n;
     const uint64_t j = a.status[ST_J];
     const uint64_t ns = merged ? k - (j + 1) : 0;
@@ -145,10 +154,15 @@ __global__ void __launch_bounds__(256) k_resync_tail(ResyncArgs a)
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *a.ncuts = m + ns;
         if (merged) a.status[ST_OVERHANG] = k ? __ldcg(a.spec + k - 1) : a.status[ST_OVERHANG];
+        if (a.sum3) {
+            a.sum3[0] = a.status[ST_OVERHANG];
+            a.sum3[1] = m + ns;
+            a.sum3[2] = *a.spec_ov;
+        }
     }
 }
 
-// Rank r's local merge with rank r-1's tail: blk = [n, overhang, e_0 .. e_{n-1}],
+// Rank r's local merge with rank r-1's tail: blk = [overhang, count, n, e_0 .. e_{n-1}],
 // the true chain from rank r's entry (e_0 = the overhang).  The first e_i that
 // is also a speculative cut of this range is a merge: the result is e_1..e_i
 // followed by the speculative cuts after it (k_resync_tail).  No merge within
@@ -156,10 +170,10 @@ __global__ void __launch_bounds__(256) k_resync_tail(ResyncArgs a)
 __global__ void __launch_bounds__(128) k_merge_tail(const uint64_t *blk, uint32_t tail_max, ResyncArgs a)
 {
     __shared__ unsigned long long best;                  // (i << 32) | j of the first merge
-    const uint64_t n = min(blk[0], (uint64_t)tail_max);
-    const uint64_t *e = blk + 2;
+    const uint64_t n = min(blk[2], (uint64_t)tail_max);
+    const uint64_t *e = blk + 3;
     const uint64_t k = *a.spec_n;
-    const uint64_t ov = blk[1];
+    const uint64_t ov = blk[0];
     if (threadIdx.x == 0) best = ~0ull;
     __syncthreads();
     if (ov >= a.gofs + a.stop) {                         // no chunk starts in this range
@@ -231,15 +245,23 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
                        const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
                        uint64_t *d_status, void *stream, const uint64_t *merge_blk = nullptr,
                        uint32_t tail_max = 0);
+static thread_local uint64_t *g_sum3 = nullptr;          // merge_tail's optional summary outputs
+static thread_local const uint64_t *g_spec_ov = nullptr;
 
 SEQCDC_API int seqcdc_range_merge_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
                                        uint64_t global_offset, const seqcdc_params_t *p, const uint64_t *d_prev,
                                        uint32_t tail_max, const uint64_t *d_spec, const uint64_t *d_spec_n,
-                                       uint64_t *d_cuts, uint64_t *d_ncuts, uint64_t *d_status, void *stream)
+                                       uint64_t *d_cuts, uint64_t *d_ncuts, uint64_t *d_status,
+                                       const uint64_t *d_spec_ov, uint64_t *d_sum3, void *stream)
 {
-    if (!d_prev) return SEQCDC_EINVAL;
-    return resync_impl(d_buf, buf_len, range_len, 0, d_prev + 1, global_offset, p, d_spec, d_spec_n, d_cuts, d_ncuts,
-                       d_status, stream, d_prev, tail_max);
+    if (!d_prev || (d_sum3 && !d_spec_ov)) return SEQCDC_EINVAL;
+    g_sum3 = d_sum3;
+    g_spec_ov = d_spec_ov;
+    const int rc = resync_impl(d_buf, buf_len, range_len, 0, d_prev, global_offset, p, d_spec, d_spec_n, d_cuts,
+                               d_ncuts, d_status, stream, d_prev, tail_max);
+    g_sum3 = nullptr;
+    g_spec_ov = nullptr;
+    return rc;
 }
 
 SEQCDC_API int seqcdc_range_resync_dev(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
@@ -281,6 +303,8 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
     a.stop = range_len;
     a.entry = entry;
     a.d_entry = d_entry;
+    a.sum3 = g_sum3;
+    a.spec_ov = g_spec_ov;
     a.gofs = global_offset;
     a.spec = d_spec;
     a.spec_n = d_spec_n;

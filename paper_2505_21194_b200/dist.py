@@ -126,10 +126,11 @@ def _device_round(shard, backend, group, P, r):
     a re-walk only if the tail is too short).  A second all_gather of
     (overhang, count, speculative overhang) gives the global prefix and proves
     no overhang changed."""
-    spec = backend.spec_dev_tail(shard, last=(r == P - 1))   # extra: "block" [2 + E], "sum" [2]
-    blocks = _allgather_dev(spec.extra["block"], group)     # [P, 2 + E]
+    spec = backend.spec_dev_tail(shard, last=(r == P - 1))   # extra: "block" [3 + E]
+    blocks = _allgather_dev(spec.extra["block"], group)     # [P, 3 + E]
     cur = backend.merge_dev(shard, blocks[r - 1], spec) if r > 0 else spec
-    info = _allgather_dev(torch.cat([cur.extra["sum"], spec.extra["sum"][0:1]]), group)   # [P, 3]
+    s3 = cur.extra["sum3"] if r > 0 else spec.extra["block"][[0, 1, 0]]   # rank 0's chain is final
+    info = _allgather_dev(s3, group)                        # [P, 3] = final ov, count, speculative ov
     h = info.reshape(-1).cpu().tolist()
     if any(h[3 * k] != h[3 * k + 2] for k in range(P)):     # an overhang changed: more rounds needed
         return None
@@ -189,7 +190,8 @@ class CudaRangeBackend:
         self.status = torch.zeros(4, dtype=torch.int64, device=dev)
         self.ws = torch.empty(workspace_size(n, 1, self.p), dtype=torch.uint8, device=dev)
         self.host = torch.empty(8, dtype=torch.int64, pin_memory=True)
-        self.block = torch.zeros(2 + self.TAIL, dtype=torch.int64, device=dev)
+        self.block = torch.zeros(3 + self.TAIL, dtype=torch.int64, device=dev)   # ov, count, tail_n, tail
+        self.sum3 = torch.zeros(3, dtype=torch.int64, device=dev)
         self._key = key
 
     def _read(self, cuts, ncuts, extra=None) -> list[int]:
@@ -255,13 +257,13 @@ class CudaRangeBackend:
         self._alloc(shard)
         E = 0 if last else self.TAIL
         with torch.cuda.device(self.device):
-            self.block[0].zero_()
+            if last:
+                self.block[2].zero_()
             range_chunk_tail_into(shard.buf, shard.range_len, shard.global_offset, self.p, self.spec_cuts,
-                                  self.spec_n, E, self.block[2:], self.block[0:1], workspace=self.ws,
-                                  stream=self.stream)
-            sm = self._summary(self.spec_cuts, self.spec_n, shard.global_offset)
-            self.block[1:2].copy_(sm[0:1])
-        return Chain(self.spec_cuts, -1, -1, {"sum": sm, "block": self.block})
+                                  self.spec_n, E, self.block, workspace=self.ws, stream=self.stream)
+        # exchange block = (overhang, count, tail_n, tail); the second exchange
+        # for rank 0 is (overhang, count, overhang): its chain is final already
+        return Chain(self.spec_cuts, -1, -1, {"block": self.block})
 
     def merge_dev(self, shard: Shard, prev_block, spec: Chain) -> Chain:
         from . import range_merge_tail_into
@@ -269,6 +271,6 @@ class CudaRangeBackend:
         with torch.cuda.device(self.device):
             pb = prev_block.contiguous()
             range_merge_tail_into(shard.buf, shard.range_len, shard.global_offset, self.p, pb, self.TAIL, spec.cuts,
-                                  self.spec_n, self.out_cuts, self.out_n, self.status, stream=self.stream)
-            sm = torch.cat([self.status[3:4], self.out_n.reshape(1)])
-        return Chain(self.out_cuts, -1, -1, {"sum": sm})
+                                  self.spec_n, self.out_cuts, self.out_n, self.status, spec_ov=self.block,
+                                  sum3=self.sum3, stream=self.stream)
+        return Chain(self.out_cuts, -1, -1, {"sum3": self.sum3})

@@ -172,13 +172,13 @@ def test_range_tail_and_local_merge(kind, seed, p):
         cap0 = sc.range_max_cuts(buf0.numel(), R[1], sp)
         c0 = torch.empty(cap0, dtype=torch.int64, device="cuda")
         n0 = torch.zeros(1, dtype=torch.int64, device="cuda")
-        blk = torch.zeros(2 + E, dtype=torch.int64, device="cuda")
-        sc.range_chunk_tail_into(buf0, R[1], 0, sp, c0, n0, tail_max, blk[2:], blk[0:1])
+        blk = torch.zeros(3 + E, dtype=torch.int64, device="cuda")
+        sc.range_chunk_tail_into(buf0, R[1], 0, sp, c0, n0, tail_max, blk)
         k0 = int(n0.item())
         ov = int(c0[k0 - 1].item())
-        blk[1] = ov
-        tn = int(blk[0].item())
-        tail = blk[2:2 + tn].cpu().numpy().astype(np.uint64)
+        assert blk[:2].cpu().tolist() == [ov, k0]          # the summary written by the library
+        tn = int(blk[2].item())
+        tail = blk[3:3 + tn].cpu().numpy().astype(np.uint64)
         # oracle: the true chain from the overhang, chunks wholly inside the buffer
         want_tail = [ov]
         base = ov
@@ -195,7 +195,11 @@ def test_range_tail_and_local_merge(kind, seed, p):
         out = torch.empty(cap1, dtype=torch.int64, device="cuda")
         out_n = torch.zeros(1, dtype=torch.int64, device="cuda")
         status = torch.zeros(4, dtype=torch.int64, device="cuda")
+        own = torch.tensor([12345], dtype=torch.int64, device="cuda")
+        sum3 = torch.zeros(3, dtype=torch.int64, device="cuda")
         sc.range_merge_tail_into(buf1, R[2] - R[1], R[1], sp, blk, E if tail_max == E else tail_max, spec, spec_n,
-                                 out, out_n, status)
+                                 out, out_n, status, spec_ov=own, sum3=sum3)
         got = out[: int(out_n.item())].cpu().numpy().astype(np.uint64)
-        assert np.array_equal(got, full[full > ov]), (kind, tail_max, status.cpu().tolist())
+        want = full[full > ov]
+        assert np.array_equal(got, want), (kind, tail_max, status.cpu().tolist())
+        assert sum3.cpu().tolist() == [int(want[-1]), int(want.size), 12345]

@@ -40,7 +40,7 @@ for it in range(8):
     ev[1].record()
     cur = be.merge_dev(shard, prev, spec)
     ev[2].record()
-    h = torch.cat([cur.extra["sum"], spec.extra["sum"]]).cpu()
+    h = cur.extra["sum3"].cpu()
     ev[3].record()
     torch.cuda.synchronize()
     if it >= 3:
@@ -49,5 +49,5 @@ m = [sum(r[i] for r in res) / len(res) for i in range(3)]
 st = be.status.cpu().tolist()
 print(json.dumps({"shard_bytes": n_per, "spec_with_tail_ms": round(m[0], 4), "merge_ms": round(m[1], 4),
                   "host_read_ms": round(m[2], 4), "merged_via_tail": st[0] == 1, "tail_cuts_used": st[1],
-                  "prev_tail_n": int(prev[0].item()),
+                  "prev_tail_n": int(prev[2].item()),
                   "note": "plus two NCCL all_gathers per step (not measurable on one GPU)"}))
