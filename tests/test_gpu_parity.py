@@ -267,3 +267,28 @@ def test_signed_flag(kind, seed):
     gc, gi = _gpu_batch(b, offs, p)
     _assert_same(gi, wi, "signed batch index")
     _assert_same(gc, wc, "signed batch")
+
+
+@pytest.mark.parametrize("G", [1 << 14, 1 << 16])
+def test_batch_overflowing_extensions(G):
+    """Batch path: phase-locked streams (no common cut between a chain started
+    at a segment start and the true chain) with small segments, so extensions
+    exhaust their budget and k_stitch continues them; mixed with normal
+    streams and empty ones."""
+    rng = np.random.default_rng(G)
+    n = 700_000
+    i = np.arange(n)
+    streams = [((255 - i) % 256).astype(np.uint8),                 # descending ramp (Increasing mode)
+               np.full(n // 2 + 7, 9, np.uint8),
+               synth.fill_host("uniform", 5, 0, n),
+               np.zeros(0, np.uint8),
+               ((255 - i[: n // 3]) % 256).astype(np.uint8)]
+    offs = np.zeros(len(streams) + 1, np.uint64)
+    offs[1:] = np.cumsum([s.size for s in streams])
+    allb = np.concatenate(streams)
+    sc.set_segment_bytes(G)
+    for p in (oracle.Params(0, 5, 50, 256, 1000, 4000), oracle.Params(0, 4, 3, 40, 300, 1111)):
+        want_c, want_i = oracle.chunk_batch(allb, offs, p)
+        got_c, got_i = _gpu_batch(allb, offs, p)
+        _assert_same(got_i, want_i, f"cut_index {p}")
+        _assert_same(got_c, want_c, f"cuts {p}")

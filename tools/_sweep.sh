@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT
-SEQCDC_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 5 --warmup 3 --bytes-per-gpu 536870912 > gpurun_out/bench_n2_gloo.log 2>&1
-echo "exit $?" >> gpurun_out/bench_n2_gloo.log
+python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "overflowing" > gpurun_out/pytest_ovf.log 2>&1
+timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "edge_sizes or unaligned_input or parameter_extremes or flat_runs_gallop" -p no:cacheprovider > gpurun_out/memcheck.log 2>&1
+echo "memcheck exit $?" >> gpurun_out/memcheck.log
