@@ -1,4 +1,9 @@
 cd $GRAFT_REPO_ROOT
-python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "overflowing" > gpurun_out/pytest_ovf.log 2>&1
-timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "edge_sizes or unaligned_input or parameter_extremes or flat_runs_gallop" -p no:cacheprovider > gpurun_out/memcheck.log 2>&1
-echo "memcheck exit $?" >> gpurun_out/memcheck.log
+python -m pytest tests/test_gpu_parity.py tests/test_gpu_range.py tests/test_gpu_dedup.py -m gpu -q -x > gpurun_out/pytest_quick.log 2>&1
+for wgt in 0 1; do
+  for i in 1 2; do SEQCDC_WEIGHTED=$wgt python tools/tune.py markov 2 1024 4 1 30 >> gpurun_out/sweep25.jsonl 2>&1; done
+  SEQCDC_WEIGHTED=$wgt python tools/tune.py markov 2 4096 4 1 10 >> gpurun_out/sweep25.jsonl 2>&1
+  SEQCDC_WEIGHTED=$wgt python tools/tune.py rampmix 5 4096 8 0 10 >> gpurun_out/sweep25.jsonl 2>&1
+  SEQCDC_WEIGHTED=$wgt python tools/tune.py uniform 1 4096 8 0 10 >> gpurun_out/sweep25.jsonl 2>&1
+done
+SEQCDC_LIB=build/v_tl.so TL_SAVE=gpurun_out/tl_w.npy python tools/timeline.py markov 2 1024 4 1 > gpurun_out/tl25.jsonl 2>&1

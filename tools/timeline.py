@@ -35,8 +35,10 @@ torch.cuda.synchronize()
 L.seqcdc_debug_timeline(None, 0)
 a = tl.cpu().numpy().reshape(-1, 4)
 a = a[a[:, 0] > 0]
+wid = a[:, 3] >> 32
+a[:, 3] &= 0xffffffff
 if os.environ.get("TL_SAVE"):
-    np.save(os.environ["TL_SAVE"], a)
+    np.save(os.environ["TL_SAVE"], np.concatenate([a, wid[:, None]], axis=1))
 t0 = a[:, 0].min()
 st, sp, ex = (a[:, 0] - t0) / 1e3, (a[:, 1] - t0) / 1e3, (a[:, 2] - t0) / 1e3
 ex = np.where(a[:, 2] > 0, ex, sp)
