@@ -274,3 +274,47 @@ class CudaRangeBackend:
                                   self.spec_n, self.out_cuts, self.out_n, self.status, spec_ov=self.block,
                                   sum3=self.sum3, stream=self.stream)
         return Chain(self.out_cuts, -1, -1, {"sum3": self.sum3})
+
+
+# ---------------------------------------------------------------- batches of independent streams
+def lpt_assign(sizes, P: int):
+    """Longest-processing-time-first assignment of whole streams to P ranks
+    ("assign whole streams to GPUs with LPT by size"): streams
+    in decreasing size, each to the currently lightest rank (ties -> lowest
+    rank).  Deterministic; returns a list of stream-index lists (ascending)."""
+    import heapq
+    order = sorted(range(len(sizes)), key=lambda j: (-int(sizes[j]), j))
+    heap = [(0, r) for r in range(P)]
+    out = [[] for _ in range(P)]
+    for j in order:
+        load, r = heapq.heappop(heap)
+        out[r].append(j)
+        heapq.heappush(heap, (load + int(sizes[j]), r))
+    return [sorted(x) for x in out]
+
+
+def chunk_batch_sharded(streams, p, group=None, device=None):
+    """Chunk this rank's share of a batch of independent streams ("files are
+    chunked independently"): no data-path collective, one all_reduce of
+    the cut totals.  ``streams`` = {stream index: uint8 CUDA tensor} for the
+    streams lpt_assign gave this rank.  Returns ({index: cuts (local offsets)},
+    total cuts over all ranks)."""
+    from . import chunk_batch
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    idx = sorted(streams)
+    out = {}
+    local = 0
+    if idx:
+        sizes = [streams[j].numel() for j in idx]
+        offs = torch.zeros(len(idx) + 1, dtype=torch.int64)
+        offs[1:] = torch.cumsum(torch.tensor(sizes, dtype=torch.int64), 0)
+        data = torch.cat([streams[j].reshape(-1) for j in idx]).to(dev)
+        cuts, ci = chunk_batch(data, offs.to(dev), p)
+        ci = ci.cpu().tolist()
+        offl = offs.tolist()
+        for t, j in enumerate(idx):
+            out[j] = cuts[ci[t]:ci[t + 1]] - offl[t]
+        local = int(ci[-1])
+    tot = torch.tensor([local], dtype=torch.int64, device=dev if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(tot, group=group)
+    return out, int(tot.item())

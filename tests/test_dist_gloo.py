@@ -100,3 +100,16 @@ def test_sharded_equals_single_stream(P, case):
     assert np.array_equal(np.asarray(got, np.uint64), want), case
     if case == "zeros" and P >= 3:
         assert max(r[3] for r in allc) >= 2      # overhang changes cascaded (several rounds)
+
+
+def test_lpt_assign_balances_and_partitions():
+    from paper_2505_21194_b200.dist import lpt_assign
+    rng = np.random.default_rng(4)
+    sizes = rng.integers(1, 1 << 26, 256)
+    for P in (1, 2, 3, 8):
+        parts = lpt_assign(sizes, P)
+        flat = sorted(j for part in parts for j in part)
+        assert flat == list(range(sizes.size))                        # every stream exactly once
+        loads = [int(sizes[part].sum()) for part in parts]
+        assert max(loads) - min(loads) <= int(sizes.max())            # LPT bound: gap <= largest job
+    assert lpt_assign([5, 5, 5], 2) == [[0, 2], [1]]

@@ -203,3 +203,56 @@ def test_range_tail_and_local_merge(kind, seed, p):
         want = full[full > ov]
         assert np.array_equal(got, want), (kind, tail_max, status.cpu().tolist())
         assert sum3.cpu().tolist() == [int(want[-1]), int(want.size), 12345]
+
+
+def _batch_worker(rank, P, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        from paper_2505_21194_b200.dist import chunk_batch_sharded, lpt_assign
+        off, kinds, seeds = synth.batch_layout(3, 24, 1 << 20)
+        sizes = np.diff(off.astype(np.int64))
+        mine = lpt_assign(sizes, P)[rank]
+        streams = {}
+        for j in mine:
+            t = torch.empty(int(sizes[j]), dtype=torch.uint8, device="cuda")
+            synth.fill_device(int(kinds[j]), int(seeds[j]), 0, t)
+            streams[j] = t
+        out, total = chunk_batch_sharded(streams, _sp(oracle.table1(8)))
+        res = {j: c.cpu().numpy().tolist() for j, c in out.items()}
+        allr = [None] * P
+        dist.all_gather_object(allr, (res, total))
+        if rank == 0:
+            q.put(allr)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_batch_sharded_lpt(P):
+    """Batches of independent streams over P ranks (LPT by size, no data-path
+    collective): per-stream cut lists = the oracle's, totals all-reduced."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, P, port, q)) for r in range(P)]
+    for pr in procs:
+        pr.start()
+    allr = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    off, kinds, seeds = synth.batch_layout(3, 24, 1 << 20)
+    p = oracle.table1(8)
+    got = {}
+    for res, total in allr:
+        got.update(res)
+    want_total = 0
+    for j in range(24):
+        b = synth.fill_host(int(kinds[j]), int(seeds[j]), 0, int(off[j + 1] - off[j]))
+        w = oracle.chunk(b, p)
+        want_total += w.size
+        assert np.array_equal(np.asarray(got[j], np.uint64), w), j
+    assert all(t == want_total for _, t in allr)
