@@ -443,14 +443,16 @@ __device__ __forceinline__ uint32_t run_mask(uint32_t Fm, uint32_t carry, uint32
 // f(base): the cut ending the chunk that starts at relative position `base`
 // (base < end_rel).  Warp-uniform; every lane returns the same value.
 //
-// One round per examined window of 128 pairs (4 per lane).  Both events are
-// located with ballots only (no shuffle-reduction on the critical path):
-//   r = first pair ending a favourable run (ballot + __ffs, "builtin_ffs")
+// One round per examined window of 128 pairs (4 per lane).  Each lane finds
+// its own candidates, a warp min-reduction (REDUX) picks the first of each:
+//   r = first pair ending a favourable run (per-lane __ffs, "builtin_ffs")
 //   d = the need-th opposing pair: per-lane exclusive prefix of the opposing
-//       counts from three count-bit ballots, the crossing lane by a ballot, the
-//       byte inside it by a SWAR prefix ("pdep + tzcnt").
+//       counts from three count-bit ballots, the crossing lane's byte by a
+//       SWAR prefix ("pdep + tzcnt").
 // r < d -> cut r+2; d < r -> skip to d+1+S with fresh counters;
 // neither -> next window.  Pairs and bytes come from the warp's ring.
+// (The min-reduction replaced ballot + ffs + shuffle: lone-walker latency
+// 0.80 -> 0.745 us per chunk, profiles/r01/sweeps.md.)
 template <int MODE, int MSPEC>
 __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint32_t base, int lane)
 {
@@ -497,10 +499,16 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
         const uint32_t cnt = __popc(Om);
         const uint32_t b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),
                        b2 = __ballot_sync(FULL, cnt & 4);
-        const uint32_t rmask = __ballot_sync(FULL, R != 0);
         const uint32_t excl = __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask);
-        const uint32_t dmask = __ballot_sync(FULL, excl + cnt >= need);
-        if ((rmask | dmask) == 0) {                // nothing decided in this window
+        // per-lane candidates, the first of each by a warp min-reduction
+        constexpr uint32_t NONE = 0xffffffffu;
+        const uint32_t rc = R ? 4 * (uint32_t)lane + ((uint32_t)(__ffs(R) - 1) >> 3) : NONE;
+        const uint32_t pcr = (Om >> 7) * 0x01010101u;
+        const uint32_t ger = ((pcr | H) - (need - excl) * 0x01010101u) & 0x00808080u;
+        const uint32_t dc = (excl < need && excl + cnt >= need) ? 4 * (uint32_t)lane + 3u - __popc(ger) : NONE;
+        const uint32_t r = __reduce_min_sync(FULL, rc);
+        const uint32_t d = __reduce_min_sync(FULL, dc);
+        if ((r & d) == NONE) {                     // nothing decided in this window
             need -= __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
             carry = MSPEC >= 0 ? __shfl_sync(FULL, Fm, 31) : Fm;
             const bool flat = !__any_sync(FULL, (Fm | Om) != 0);
@@ -531,16 +539,6 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
             }
             continue;
         }
-        // per lane: byte of its first run end, byte of its k-th opposing pair
-        // (k = need - excl; byte j of pc = opposing flags in bytes 0..j)
-        const uint32_t rbyte = (uint32_t)(__ffs(R) - 1) >> 3;
-        const uint32_t pc = (Om >> 7) * 0x01010101u;
-        const uint32_t ge = ((pc | H) - (need - excl) * 0x01010101u) & 0x00808080u;
-        const uint32_t dbyte = 3u - __popc(ge);
-        const uint32_t rl = rmask ? (uint32_t)__ffs(rmask) - 1 : 32u;
-        const uint32_t dl = dmask ? (uint32_t)__ffs(dmask) - 1 : 32u;
-        const uint32_t r = 4 * rl + __shfl_sync(FULL, rbyte, rl & 31);
-        const uint32_t d = 4 * dl + __shfl_sync(FULL, dbyte, dl & 31);
         if (r < d) {                               // the run completes first: boundary after it
             const uint32_t ra = p0 + r;
             return ra <= lim2 ? ra + 2 : limit;
