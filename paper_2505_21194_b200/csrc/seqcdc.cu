@@ -418,6 +418,10 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
     int64_t mi = -1;
     uint64_t t_lo = 0, t_Loff = 0;
     const uint32_t ext_end = hi_rel + (uint32_t)(K_EXT * w.G);  // byte budget (REL_CLAMP safety)
+    // segment owning the current cut, tracked incrementally (segments are uniform
+    // within a stream: segment t starts at S0 + (t - first) * G)
+    uint32_t t = s;
+    uint64_t t_next = seg_start(w, g, s + 1);
 #pragma unroll 1
     for (;;) {
         if (xb.n == g.Xcap || c > ext_end) {
@@ -430,7 +434,11 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
             tgt = TGT_END;
             break;
         }
-        const uint32_t t = g.first + (uint32_t)((cut - g.S0) / w.G);
+#pragma unroll 1
+        while (cut >= t_next) {
+            t++;
+            t_next += w.G;
+        }
         if ((int64_t)t != cur.t) {
             t_lo = seg_start(w, g, t);
             t_Loff = w.single ? (uint64_t)t * w.capL1 : w.Loff[t];
@@ -483,6 +491,8 @@ __device__ uint32_t continue_chain(const Work &w, Walker &wk, const Seg &g, uint
     mi = -1;
     uint64_t pos = from;
     bool done = false;
+    uint32_t t = g.first + (uint32_t)((from - g.S0) / w.G);     // segment owning `from`, then incremental
+    uint64_t t_next = seg_start(w, g, t + 1);
 #pragma unroll 1
     while (!done && pos < stop) {
         uint32_t base = walker_begin(wk, abase + pos, abase + g.E);
@@ -498,7 +508,11 @@ __device__ uint32_t continue_chain(const Work &w, Walker &wk, const Seg &g, uint
                 done = true;
                 break;
             }
-            const uint32_t t = g.first + (uint32_t)((cut - g.S0) / w.G);
+#pragma unroll 1
+            while (cut >= t_next) {
+                t++;
+                t_next += w.G;
+            }
             if ((int64_t)t != cur.t) {
                 t_lo = seg_start(w, g, t);
                 t_Loff = w.single ? (uint64_t)t * w.capL1 : w.Loff[t];
