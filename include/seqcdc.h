@@ -62,6 +62,12 @@ extern "C" {
 /* seqcdc_params_t.flags: compare bytes as SIGNED int8 instead of unsigned
  * (the alternative reading of P:215's untyped mm512_cmpgt; DESIGN.md c6). */
 #define SEQCDC_FLAG_SIGNED 1u
+/* seqcdc_params_t.flags: SeqLength counts favourable COMPARISONS instead of
+ * bytes (the alternative reading of P:153, DESIGN.md c1): a chunk ends after a
+ * run of L favourable pairs (L+1 bytes); scanning still starts at chunk start
+ * + min - L.  Equivalent to the bytes reading with (L+1, min+1).
+ * L <= SEQCDC_MAX_SEQ_LENGTH - 1 with this flag. */
+#define SEQCDC_FLAG_PAIRS 2u
 
 /* Written to *d_ncuts if the device detects inconsistent batch offsets
  * (non-monotone, or d_offsets[ns]-d_offsets[0] != total_bytes). */
@@ -77,13 +83,13 @@ typedef struct seqcdc_params {
                                byte; 0 disables skipping                    */
     uint64_t min_size;      /* >= L; scanning starts at chunk start + min - L */
     uint64_t max_size;      /* >= min_size; forced cut                        */
-    uint32_t flags;         /* 0, or SEQCDC_FLAG_SIGNED                              */
+    uint32_t flags;         /* 0, or SEQCDC_FLAG_SIGNED | SEQCDC_FLAG_PAIRS          */
     uint32_t reserved;      /* must be 0                                             */
 } seqcdc_params_t;
 
 /* SEQCDC_OK if *p is acceptable, SEQCDC_EINVAL otherwise (mode not 0/1,
- * L < 2 or L > SEQCDC_MAX_SEQ_LENGTH, T == 0, min < L, max < min, unknown
- * flags, reserved != 0, p == NULL). */
+ * L < 2 or L > SEQCDC_MAX_SEQ_LENGTH (- 1 with SEQCDC_FLAG_PAIRS), T == 0,
+ * min < L, max < min, unknown flags, reserved != 0, p == NULL). */
 int seqcdc_validate_params(const seqcdc_params_t *p);
 
 /* Table I row for avg_kib in {4, 8, 16} with min = avg/2 and

@@ -48,6 +48,16 @@ class Params:
     min_size: int = 4096
     max_size: int = 16384
     signed: bool = False            # compare bytes as int8 (reading c6's alternative)
+    pairs: bool = False             # L counts favourable comparisons (reading c1's alternative)
+
+    @property
+    def flags(self) -> int:
+        return int(self.signed) | (2 if self.pairs else 0)
+
+    @property
+    def run_bytes(self) -> int:
+        """Bytes in a qualifying run: L (c1), or L+1 when L counts comparisons."""
+        return self.seq_length + 1 if self.pairs else self.seq_length
 
     def check(self) -> None:
         if self.mode not in (0, 1):
@@ -116,7 +126,7 @@ def chunk(data, p: Params, return_examined: bool = False):
     cuts = np.empty(cap, dtype=np.uint64)
     ex = ctypes.c_uint64(0)
     k = _load().oracle_chunk(b.ctypes.data, n, p.mode, p.seq_length, p.skip_trigger,
-                             p.skip_size, p.min_size, p.max_size, int(p.signed), cuts.ctypes.data, cap,
+                             p.skip_size, p.min_size, p.max_size, p.flags, cuts.ctypes.data, cap,
                              ctypes.addressof(ex))
     if k < 0:
         raise RuntimeError(f"oracle_chunk failed ({k})")
@@ -131,7 +141,7 @@ def next_cut(data, base: int, p: Params) -> int:
         raise ValueError("base out of range")
     return int(_load().oracle_next_cut(b.ctypes.data, b.size, base, p.mode, p.seq_length,
                                        p.skip_trigger, p.skip_size, p.min_size, p.max_size,
-                                       int(p.signed), None))
+                                       p.flags, None))
 
 
 def chunk_batch(data, offsets, p: Params):
@@ -145,7 +155,7 @@ def chunk_batch(data, offsets, p: Params):
     idx = np.empty(ns + 1, dtype=np.uint64)
     k = _load().oracle_chunk_batch(b.ctypes.data, off.ctypes.data, ns, p.mode, p.seq_length,
                                    p.skip_trigger, p.skip_size, p.min_size, p.max_size,
-                                   int(p.signed), cuts.ctypes.data, cap, idx.ctypes.data)
+                                   p.flags, cuts.ctypes.data, cap, idx.ctypes.data)
     if k < 0:
         raise RuntimeError(f"oracle_chunk_batch failed ({k})")
     return cuts[:k].copy(), idx
@@ -159,6 +169,7 @@ def chunk_py(data, p: Params) -> list:
     b = bytes(_as_u8(data))
     n = len(b)
     L, T, S = p.seq_length, p.skip_trigger, p.skip_size
+    run_end = p.run_bytes                          # c1 (bytes) or its comparisons alternative
     cuts, base = [], 0
     while base < n:
         limit = min(base + p.max_size, n)
@@ -175,7 +186,7 @@ def chunk_py(data, p: Params) -> list:
             opn = x > y if p.mode == INCREASING else x < y
             if fav:
                 run += 1
-                if run == L:
+                if run == run_end:
                     cut = i + 2
                     break
                 i += 1
@@ -216,9 +227,10 @@ def chunk_query(data, p: Params) -> np.ndarray:
         fav, opn = diff > 0, diff < 0
     else:
         fav, opn = diff < 0, diff > 0
-    # run_start[k] = bytes k..k+L-1 strictly monotone  <=> fav[k..k+L-2] all set
+    # run_start[k] = bytes k..k+Lb-1 strictly monotone  <=> fav[k..k+Lb-2] all set
+    # (Lb = bytes per qualifying run: L, or L+1 when L counts comparisons)
     cs = np.concatenate([[0], np.cumsum(fav, dtype=np.int64)])
-    m = L - 1
+    m = p.run_bytes - 1
     npairs = fav.size
     if npairs >= m:
         ks = np.arange(0, npairs - m + 1)
@@ -245,7 +257,7 @@ def chunk_query(data, p: Params) -> np.ndarray:
             if d is not None and d > last_pair:
                 d = None
             if k is not None and (d is None or k + m - 1 < d):
-                cut = k + L
+                cut = k + m + 1
                 break
             if d is not None:
                 a = d + 1 + S

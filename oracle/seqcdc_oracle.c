@@ -33,8 +33,11 @@
  * the second byte of the triggering pair, i.e. at d+1+S (c3); both counters
  * reset at chunk start and after a skip, the run also resets on any
  * non-favourable pair (c4); equal bytes set neither flag (c5); bytes compare
- * as UNSIGNED (c6; `sgn` = 1 selects the signed reading, P:215's
- * mm512_cmpgt without a type suffix could be the signed epi8 compare); skipped bytes count toward max and a skip landing past the
+ * as UNSIGNED (c6; `flags` bit 0 selects the signed reading, P:215's
+ * mm512_cmpgt without a type suffix could be the signed epi8 compare; `flags`
+ * bit 1 selects c1's alternative: SeqLength counts favourable comparisons, so
+ * a run of L+1 bytes ends a chunk, the scan anchor staying at base + min - L);
+ * skipped bytes count toward max and a skip landing past the
  * limit gives the limit (c8); the last chunk may be shorter than min and the
  * last cut is n; n == 0 gives no cuts (c9).
  *
@@ -69,8 +72,10 @@ int oracle_check_params(uint32_t mode, uint32_t seq_length, uint32_t skip_trigge
 uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
                          uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
                          uint32_t skip_size, uint64_t min_size, uint64_t max_size,
-                         uint32_t sgn, uint64_t *examined)
+                         uint32_t flags, uint64_t *examined)
 {
+    const uint32_t sgn = flags & 1u;               /* signed bytes (c6 alternative) */
+    const uint32_t run_end = (flags & 2u) ? seq_length + 1 : seq_length;   /* bytes in a qualifying run (c1) */
     uint64_t limit = base + max_size;              /* P:266 max forced cut */
     if (limit > n) limit = n;                      /* end of stream (c9) */
     uint64_t i = base + min_size - seq_length;     /* P:179 sub-minimum skip */
@@ -86,7 +91,7 @@ uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
         else           { favourable = x > y; opposing = x < y; }   /* Decreasing */
         if (favourable) {
             run += 1;
-            if (run == seq_length) return i + 2;   /* run ends at byte i+1 -> cut after it */
+            if (run == run_end) return i + 2;      /* run ends at byte i+1 -> cut after it */
             i += 1;
         } else if (opposing) {
             run = 1;
@@ -113,14 +118,14 @@ uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
 int64_t oracle_chunk(const uint8_t *b, uint64_t n,
                      uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
                      uint32_t skip_size, uint64_t min_size, uint64_t max_size,
-                     uint32_t sgn, uint64_t *cuts, uint64_t cap, uint64_t *examined)
+                     uint32_t flags, uint64_t *cuts, uint64_t cap, uint64_t *examined)
 {
     if (oracle_check_params(mode, seq_length, skip_trigger, min_size, max_size))
         return -ORACLE_EINVAL;
     uint64_t k = 0, base = 0;
     while (base < n) {
         uint64_t c = oracle_next_cut(b, n, base, mode, seq_length, skip_trigger,
-                                     skip_size, min_size, max_size, sgn, examined);
+                                     skip_size, min_size, max_size, flags, examined);
         if (k >= cap) return -ORACLE_ECAP;
         cuts[k++] = c;
         base = c;
@@ -137,14 +142,14 @@ int64_t oracle_chunk(const uint8_t *b, uint64_t n,
 int64_t oracle_chunk_batch(const uint8_t *b, const uint64_t *offsets, uint32_t ns,
                            uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
                            uint32_t skip_size, uint64_t min_size, uint64_t max_size,
-                           uint32_t sgn, uint64_t *cuts, uint64_t cap, uint64_t *cut_index)
+                           uint32_t flags, uint64_t *cuts, uint64_t cap, uint64_t *cut_index)
 {
     uint64_t total = 0;
     for (uint32_t j = 0; j < ns; j++) {
         cut_index[j] = total;
         uint64_t lo = offsets[j], hi = offsets[j + 1];
         int64_t k = oracle_chunk(b + lo, hi - lo, mode, seq_length, skip_trigger, skip_size,
-                                 min_size, max_size, sgn, cuts + total, cap - total, NULL);
+                                 min_size, max_size, flags, cuts + total, cap - total, NULL);
         if (k < 0) return k;
         for (int64_t q = 0; q < k; q++) cuts[total + q] += lo;
         total += (uint64_t)k;

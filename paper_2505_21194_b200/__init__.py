@@ -21,6 +21,7 @@ from . import _build
 INCREASING = 0
 DECREASING = 1
 FLAG_SIGNED = 1
+FLAG_PAIRS = 2      # SeqLength counts favourable comparisons (reading c1's alternative)
 
 SEQCDC_OK, SEQCDC_EINVAL, SEQCDC_ENOMEM, SEQCDC_ECUDA = 0, 1, 2, 3
 NCUTS_BAD_INPUT = (1 << 64) - 1
@@ -53,7 +54,7 @@ class SeqParams:
     skip_size: int = 256
     min_size: int = 4096
     max_size: int = 16384
-    flags: int = 0          # SEQCDC_FLAG_SIGNED (1): int8 byte order
+    flags: int = 0          # SEQCDC_FLAG_SIGNED (1): int8 byte order; SEQCDC_FLAG_PAIRS (2): L comparisons
 
     def c(self) -> _CParams:
         return _CParams(self.mode, self.seq_length, self.skip_trigger, self.skip_size,

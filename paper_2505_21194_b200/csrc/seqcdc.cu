@@ -1157,7 +1157,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.p.L = p->seq_length;
     w.p.T = p->skip_trigger;
     w.p.S = p->skip_size;
-    w.p.M = p->seq_length - 1;
+    w.p.M = p->seq_length - ((p->flags & SEQCDC_FLAG_PAIRS) ? 0u : 1u);   // favourable pairs per run (c1)
     w.p.mn = (uint32_t)p->min_size;
     w.p.mx = (uint32_t)p->max_size;
     w.p.mnL = (uint32_t)p->min_size - p->seq_length;
@@ -1208,7 +1208,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     } else {
         k_setup<<<1, 1024, 0, st>>>(w);
     }
-    const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
+    const int ms = w.p.M == 4 ? 4 : (w.p.M < 4 ? 0 : -1);
     // MODE: bit 0 = Decreasing, bit 1 = signed-byte reading (flag)
     switch (p->mode | ((p->flags & SEQCDC_FLAG_SIGNED) ? 2u : 0u)) {
     case 0: launch_ms<0>(ms, w, pl, sms, st, pr); break;
@@ -1285,7 +1285,8 @@ SEQCDC_API int seqcdc_validate_params(const seqcdc_params_t *p)
     if (p->min_size < p->seq_length) return SEQCDC_EINVAL;
     if (p->max_size < p->min_size) return SEQCDC_EINVAL;
     if (p->max_size > (1ull << 28)) return SEQCDC_EINVAL;  // implementation limit: 256 MiB chunks
-    if ((p->flags & ~SEQCDC_FLAG_SIGNED) || p->reserved) return SEQCDC_EINVAL;
+    if ((p->flags & ~(SEQCDC_FLAG_SIGNED | SEQCDC_FLAG_PAIRS)) || p->reserved) return SEQCDC_EINVAL;
+    if ((p->flags & SEQCDC_FLAG_PAIRS) && p->seq_length > SEQCDC_MAX_SEQ_LENGTH - 1) return SEQCDC_EINVAL;
     return SEQCDC_OK;
 }
 

@@ -314,7 +314,7 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
     a.p.L = p->seq_length;
     a.p.T = p->skip_trigger;
     a.p.S = p->skip_size;
-    a.p.M = p->seq_length - 1;
+    a.p.M = p->seq_length - ((p->flags & SEQCDC_FLAG_PAIRS) ? 0u : 1u);
     a.p.mn = (uint32_t)p->min_size;
     a.p.mx = (uint32_t)p->max_size;
     a.p.mnL = (uint32_t)p->min_size - p->seq_length;
@@ -323,7 +323,7 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
         k_merge_tail<<<1, 128, 0, st>>>(merge_blk, tail_max, a);
         a.skip = d_status;
     }
-    const int ms = p->seq_length == 5 ? 4 : (p->seq_length < 5 ? 0 : -1);
+    const int ms = a.p.M == 4 ? 4 : (a.p.M < 4 ? 0 : -1);
     switch (p->mode | ((p->flags & SEQCDC_FLAG_SIGNED) ? 2u : 0u)) {
     case 0: launch_ms<0>(ms, a, st); break;
     case 1: launch_ms<1>(ms, a, st); break;

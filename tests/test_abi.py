@@ -49,6 +49,11 @@ def test_validate_params():
         assert not sc.validate(p), p
     assert sc.validate(sc.SeqParams(seq_length=16, min_size=16, max_size=16))
     assert sc.validate(sc.SeqParams(seq_length=2, skip_trigger=1, skip_size=0, min_size=2, max_size=2))
+    # flags: signed and comparisons readings; the latter needs L+1 <= 16 bytes per run
+    assert sc.validate(sc.SeqParams(flags=sc.FLAG_SIGNED | sc.FLAG_PAIRS))
+    assert sc.validate(sc.SeqParams(seq_length=15, min_size=16, max_size=16, flags=sc.FLAG_PAIRS))
+    assert not sc.validate(sc.SeqParams(seq_length=16, min_size=16, max_size=16, flags=sc.FLAG_PAIRS))
+    assert not sc.validate(sc.SeqParams(flags=4))
 
 
 def test_default_params_table1():

@@ -20,7 +20,7 @@ import paper_2505_21194_b200 as sc  # noqa: E402
 def _sp(p: oracle.Params) -> sc.SeqParams:
     # the two sides keep separate parameter types on purpose (no shared code)
     return sc.SeqParams(p.mode, p.seq_length, p.skip_trigger, p.skip_size, p.min_size, p.max_size,
-                        sc.FLAG_SIGNED if p.signed else 0)
+                        (sc.FLAG_SIGNED if p.signed else 0) | (sc.FLAG_PAIRS if p.pairs else 0))
 
 
 def _dev(b: np.ndarray):
@@ -292,3 +292,23 @@ def test_batch_overflowing_extensions(G):
         got_c, got_i = _gpu_batch(allb, offs, p)
         _assert_same(got_i, want_i, f"cut_index {p}")
         _assert_same(got_c, want_c, f"cuts {p}")
+
+
+@pytest.mark.parametrize("kind,seed", [("uniform", 51), ("markov", 52), ("zeroheavy", 53)])
+def test_pairs_flag(kind, seed):
+    """SEQCDC_FLAG_PAIRS (SeqLength counts comparisons, DESIGN.md c1 alternative)
+    against the oracle's comparisons reading: L = 4 (the 4-pair fast path), 5
+    and 9 (general run masks), 2 (short runs), single stream and batch."""
+    import dataclasses
+    b = synth.fill_host(kind, seed, 0, 6 << 20)
+    for p0 in (oracle.table1(4, 1), oracle.table1(8), oracle.Params(0, 4, 50, 256, 4096, 16384),
+               oracle.Params(1, 9, 30, 100, 2048, 8192), oracle.Params(0, 2, 7, 33, 300, 2000)):
+        p = dataclasses.replace(p0, pairs=True)
+        want = oracle.chunk(b, p)
+        _assert_same(_gpu_chunk(b, p), want, f"pairs {p}")
+    offs = np.array([0, 777, 400000, 3 << 20, 6 << 20], np.uint64)
+    p = dataclasses.replace(oracle.table1(8), pairs=True)
+    wc, wi = oracle.chunk_batch(b, offs, p)
+    gc, gi = _gpu_batch(b, offs, p)
+    _assert_same(gi, wi, "pairs batch index")
+    _assert_same(gc, wc, "pairs batch")

@@ -371,3 +371,46 @@ def test_fig3_block_signed_reading(golden):
     p = oracle.Params(int(g["mode"][0]), int(g["seq_length"][0]), int(g["skip_trigger"][0]),
                       int(g["skip_size"][0]), int(g["min_size"][0]), int(g["max_size"][0]), True)
     assert int(oracle.chunk(b, p)[0]) == 63
+
+
+def test_pairs_reading_closed_form_on_a_ramp():
+    """Flag for reading c1's alternative (SeqLength counts favourable comparisons,
+    P:153): on a strictly increasing stream every pair is favourable, so under
+    the bytes reading each chunk is exactly min bytes (anchor base+min-L, run of
+    L bytes ends at base+min) and under the comparisons reading min+1 (L
+    favourable pairs = L+1 bytes from the same anchor)."""
+    b = np.arange(256, dtype=np.uint8)
+    for L in (2, 4, 5, 7):
+        for mn in (L, 20, 33):
+            pb = oracle.Params(0, L, 1000, 0, mn, 64)
+            pp = oracle.Params(0, L, 1000, 0, mn, 64, pairs=True)
+            wb = list(range(mn, 256, mn)) + [256]
+            wp = list(range(mn + 1, 256, mn + 1)) + [256]
+            assert oracle.chunk(b, pb).tolist() == wb
+            assert oracle.chunk(b, pp).tolist() == wp
+            assert oracle.chunk_py(b, pp) == wp
+            assert oracle.chunk_query(b, pp).tolist() == wp
+
+
+def test_pairs_reading_is_bytes_reading_shifted():
+    """The comparisons reading with (L, min) examines the same anchor (base+min-L)
+    and needs L+1 monotone bytes, i.e. the bytes reading with (L+1, min+1): the
+    flag must match that parameter shift exactly, in all three formulations, in
+    both modes and with skipping (a dropped +1 on either the run or the anchor
+    fails here)."""
+    rng = np.random.default_rng(12)
+    for trial in range(200):
+        n = int(rng.integers(0, 3000))
+        alpha = int(rng.choice([2, 3, 8, 256]))
+        b = rng.integers(0, alpha, n).astype(np.uint8)
+        L = int(rng.integers(2, 7))
+        mn = int(rng.integers(L, L + 60))
+        mx = int(rng.integers(mn + 1, mn + 300))
+        mode, T, S = int(rng.integers(0, 2)), int(rng.integers(1, 40)), int(rng.integers(0, 90))
+        pp = oracle.Params(mode, L, T, S, mn, mx, pairs=True)
+        pb = oracle.Params(mode, L + 1, T, S, mn + 1, mx)
+        want = oracle.chunk(b, pb)
+        assert np.array_equal(oracle.chunk(b, pp), want)
+        if n <= 600:
+            assert oracle.chunk_py(b, pp) == want.tolist()
+            assert np.array_equal(oracle.chunk_query(b, pp), want)
