@@ -267,6 +267,46 @@ int seqcdc_range_merge_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t ran
                             uint64_t *d_ncuts, uint64_t *d_status, const uint64_t *d_spec_ov, uint64_t *d_sum3,
                             void *stream);
 
+/* Fused exchange over peer memory ("fused alternative": the
+ * overhang block is published from inside the producing kernel instead of by
+ * an NCCL all_gather).
+ *
+ * seqcdc_xchg_alloc: a zeroed device buffer of `bytes` for this rank's
+ * mailbox (cudaMalloc, owned by the caller until seqcdc_xchg_free) and its
+ * SEQCDC_IPC_HANDLE_BYTES-byte CUDA IPC handle (written to ipc_handle) for the
+ * other processes.  seqcdc_xchg_open maps another process's mailbox (same
+ * node; peer access over NVLink is enabled lazily) into this process:
+ * *d_peer is writable from kernels until seqcdc_xchg_close.  A process cannot
+ * open its own handle (SEQCDC_ECUDA).
+ *
+ * seqcdc_range_chunk_tail_push: seqcdc_range_chunk_tail (d_summary required)
+ * whose final kernel also stores the block [overhang, number of cuts, tail_n,
+ * tail[0..tail_n)] into d_peer_blk (a mapped peer mailbox, 3 + tail_max
+ * uint64) and then releases flag_value to *d_peer_flag at system scope.
+ *
+ * seqcdc_range_merge_tail_wait: seqcdc_range_merge_tail whose first kernel
+ * waits (on the device, no host sync) until *d_flag >= flag_value (acquire,
+ * system scope), then reads the previous range's block from d_mailbox.  After
+ * timeout_ns without the flag it reports an empty range with overhang
+ * UINT64_MAX, so d_sum3[0] != d_sum3[2] and the caller falls back to the
+ * collective protocol.  flag_value must increase from call to call (a step
+ * counter); the mailbox is reused. */
+#define SEQCDC_IPC_HANDLE_BYTES 64
+int seqcdc_xchg_alloc(size_t bytes, void **d_buf, void *ipc_handle);
+int seqcdc_xchg_open(const void *ipc_handle, void **d_peer);
+int seqcdc_xchg_close(void *d_peer);
+int seqcdc_xchg_free(void *d_buf);
+int seqcdc_range_chunk_tail_push(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                                 uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
+                                 uint64_t *d_ncuts, uint32_t tail_max, uint64_t *d_tail, uint64_t *d_tail_n,
+                                 uint64_t *d_summary, void *d_workspace, size_t ws_bytes, uint64_t *d_peer_blk,
+                                 uint64_t *d_peer_flag, uint64_t flag_value, void *stream);
+int seqcdc_range_merge_tail_wait(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t global_offset,
+                                 const seqcdc_params_t *p, const uint64_t *d_mailbox, uint32_t tail_max,
+                                 const uint64_t *d_spec, const uint64_t *d_spec_n, uint64_t *d_cuts,
+                                 uint64_t *d_ncuts, uint64_t *d_status, const uint64_t *d_spec_ov, uint64_t *d_sum3,
+                                 const uint64_t *d_flag, uint64_t flag_value, uint64_t timeout_ns, void *stream);
+
 /* Testing / tuning knob: force the segment length G (rounded up to a
  * multiple of max_size, and to at least max_size) used to split streams into
  * speculative chains; 0 restores the automatic choice.  Process-global.  The

@@ -33,6 +33,8 @@ EXPORTS = (
     "seqcdc_build_info", "seqcdc_set_segment_bytes", "seqcdc_profile_enable", "seqcdc_profile_collect",
     "seqcdc_range_max_cuts", "seqcdc_range_chunk", "seqcdc_range_resync", "seqcdc_range_resync_dev",
     "seqcdc_range_chunk_tail", "seqcdc_range_merge_tail",
+    "seqcdc_xchg_alloc", "seqcdc_xchg_open", "seqcdc_xchg_close", "seqcdc_xchg_free",
+    "seqcdc_range_chunk_tail_push", "seqcdc_range_merge_tail_wait",
     "seqcdc_fingerprint", "seqcdc_dedup_workspace_size", "seqcdc_dedup",
 )
 
@@ -122,6 +124,18 @@ def lib():
         L.seqcdc_range_chunk_tail.restype = ctypes.c_int
         L.seqcdc_range_merge_tail.argtypes = [p, u64, u64, u64, P, p, u32, p, p, p, p, p, p, p, p]
         L.seqcdc_range_merge_tail.restype = ctypes.c_int
+        L.seqcdc_xchg_alloc.argtypes = [sz, ctypes.POINTER(p), p]
+        L.seqcdc_xchg_alloc.restype = ctypes.c_int
+        L.seqcdc_xchg_open.argtypes = [p, ctypes.POINTER(p)]
+        L.seqcdc_xchg_open.restype = ctypes.c_int
+        L.seqcdc_xchg_close.argtypes = [p]
+        L.seqcdc_xchg_close.restype = ctypes.c_int
+        L.seqcdc_xchg_free.argtypes = [p]
+        L.seqcdc_xchg_free.restype = ctypes.c_int
+        L.seqcdc_range_chunk_tail_push.argtypes = [p, u64, u64, u64, u64, P, p, p, u32, p, p, p, p, sz, p, p, u64, p]
+        L.seqcdc_range_chunk_tail_push.restype = ctypes.c_int
+        L.seqcdc_range_merge_tail_wait.argtypes = [p, u64, u64, u64, P, p, u32, p, p, p, p, p, p, p, p, u64, u64, p]
+        L.seqcdc_range_merge_tail_wait.restype = ctypes.c_int
         L.seqcdc_fingerprint.argtypes = [p, p, p, u64, p, p]
         L.seqcdc_fingerprint.restype = ctypes.c_int
         L.seqcdc_dedup_workspace_size.argtypes = [u64]
@@ -363,3 +377,70 @@ def range_merge_tail_into(buf, range_len: int, global_offset: int, p: SeqParams,
                                        status.data_ptr(), spec_ov.data_ptr() if spec_ov is not None else None,
                                        sum3.data_ptr() if sum3 is not None else None, _stream_ptr(stream, buf.device))
     _check(rc, "seqcdc_range_merge_tail")
+
+
+# ---------------------------------------------------------------- fused exchange over peer memory
+IPC_HANDLE_BYTES = 64
+
+
+def xchg_alloc(nbytes: int):
+    """A zeroed device mailbox of ``nbytes`` owned by this process (free with
+    xchg_free) and its CUDA IPC handle (bytes) for the other ranks."""
+    ptr = ctypes.c_void_p()
+    h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+    _check(lib().seqcdc_xchg_alloc(int(nbytes), ctypes.byref(ptr), h), "seqcdc_xchg_alloc")
+    return int(ptr.value), bytes(h.raw)
+
+
+def xchg_open(handle: bytes) -> int:
+    """Map another process's mailbox; returns its device address in this process."""
+    if len(handle) != IPC_HANDLE_BYTES:
+        raise SeqCDCError("IPC handle must be 64 bytes")
+    ptr = ctypes.c_void_p()
+    _check(lib().seqcdc_xchg_open(handle, ctypes.byref(ptr)), "seqcdc_xchg_open")
+    return int(ptr.value)
+
+
+def xchg_close(peer_ptr: int) -> None:
+    _check(lib().seqcdc_xchg_close(peer_ptr), "seqcdc_xchg_close")
+
+
+def xchg_free(ptr: int) -> None:
+    _check(lib().seqcdc_xchg_free(ptr), "seqcdc_xchg_free")
+
+
+def range_chunk_tail_push_into(buf, range_len: int, global_offset: int, p: SeqParams, cuts, ncuts, tail_max: int,
+                               block, peer_blk: int, peer_flag: int, flag_value: int, workspace=None,
+                               stream=None) -> None:
+    """range_chunk_tail_into whose last kernel also stores the exchange block
+    into a mapped peer mailbox (``peer_blk``, 3 + tail_max int64) and releases
+    ``flag_value`` to ``peer_flag`` (device addresses from xchg_open)."""
+    _require_cuda(buf, "buf")
+    cp = p.c()
+    ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
+    b0 = block.data_ptr()
+    rc = lib().seqcdc_range_chunk_tail_push(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len, 0,
+                                            global_offset, ctypes.byref(cp),
+                                            cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(), tail_max,
+                                            b0 + 24 if tail_max else None, b0 + 16 if tail_max else None, b0,
+                                            ws_ptr, ws_len, peer_blk, peer_flag, int(flag_value),
+                                            _stream_ptr(stream, buf.device))
+    _check(rc, "seqcdc_range_chunk_tail_push")
+
+
+def range_merge_tail_wait_into(buf, range_len: int, global_offset: int, p: SeqParams, mailbox: int, flag: int,
+                               flag_value: int, tail_max: int, spec, spec_n, cuts, ncuts, status, spec_ov=None,
+                               sum3=None, timeout_ns: int = 2_000_000_000, stream=None) -> None:
+    """range_merge_tail_into reading the previous range's block from this rank's
+    mailbox (device address) once ``flag`` reaches ``flag_value`` (waited for on
+    the device; a timeout reports overhang UINT64_MAX in ``sum3``)."""
+    _require_cuda(buf, "buf")
+    cp = p.c()
+    rc = lib().seqcdc_range_merge_tail_wait(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len,
+                                            global_offset, ctypes.byref(cp), mailbox, tail_max,
+                                            spec.data_ptr() if spec.numel() else None, spec_n.data_ptr(),
+                                            cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(),
+                                            status.data_ptr(), spec_ov.data_ptr() if spec_ov is not None else None,
+                                            sum3.data_ptr() if sum3 is not None else None, flag, int(flag_value),
+                                            int(timeout_ns), _stream_ptr(stream, buf.device))
+    _check(rc, "seqcdc_range_merge_tail_wait")

@@ -95,6 +95,10 @@ struct Work {
     uint64_t *tail_n;      // count written (0 = none / invalid)
     uint32_t tail_max;
     uint64_t *summary;     // range calls (optional): [overhang, number of cuts], written by k_post
+    // range calls (optional): push the exchange block [overhang, count, tail_n, tail...]
+    // into the next range's mailbox (peer memory), then release push_value to *push_flag
+    uint64_t *push_blk, *push_flag;
+    uint64_t push_value;
 };
 
 struct Seg {
@@ -859,6 +863,20 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
         w.cut_index[1] = total;
         *w.ncuts = total;
     }
+    if (blockIdx.x == 0 && w.push_blk) {
+        // fused exchange: this range's block goes straight into the next range's
+        // mailbox over peer memory (NVLink), then the flag is released at system
+        // scope; the next range's merge kernel acquires it (SURVEY 8(e) fused form)
+        __syncthreads();                        // thread 0's summary / tail_n writes
+        const uint64_t tn = w.tail_n ? min(*(volatile uint64_t *)w.tail_n, (uint64_t)w.tail_max) : 0;
+        for (uint32_t i = tid; i < 3 + tn; i += blockDim.x)
+            w.push_blk[i] = i == 0 ? w.summary[0] : i == 1 ? w.summary[1] : i == 2 ? tn : __ldcg(w.tail + (i - 3));
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(w.push_flag), "l"(w.push_value) : "memory");
+        }
+    }
     // copy: one warp per segment
     const uint32_t nw = gridDim.x * (blockDim.x >> 5);
     for (uint32_t s2 = blockIdx.x * (blockDim.x >> 5) + wid; s2 < k; s2 += nw) {
@@ -880,6 +898,16 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
             for (uint64_t i = lane; i < nc; i += 32) out[nl + nx + i] = __ldcg(Cs + i) + add;
         }
     }
+}
+
+// an empty range's exchange block (no walk ran): [overhang, 0, 0] + flag
+__global__ void k_push_empty(uint64_t *blk, uint64_t *flag, uint64_t ov, uint64_t value)
+{
+    blk[0] = ov;
+    blk[1] = 0;
+    blk[2] = 0;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
 }
 
 __global__ void k_set2(uint64_t *p, uint64_t a, uint64_t b)
@@ -1124,6 +1152,8 @@ struct TailReq {
     uint64_t *tail = nullptr, *tail_n = nullptr;
     uint32_t max = 0;
     uint64_t *summary = nullptr;
+    uint64_t *push_blk = nullptr, *push_flag = nullptr;
+    uint64_t push_value = 0;
 };
 
 template <int MODE>
@@ -1191,6 +1221,9 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.tail_n = tail.tail_n;
     w.tail_max = tail.max;
     w.summary = tail.summary;
+    w.push_blk = tail.push_blk;
+    w.push_flag = tail.push_flag;
+    w.push_value = tail.push_value;
     if (tail.max && cudaMemsetAsync(tail.tail_n, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
 
     ProfRec rec, *pr = nullptr;
@@ -1372,19 +1405,22 @@ SEQCDC_API uint64_t seqcdc_range_max_cuts(uint64_t buf_len, uint64_t range_len, 
     return span / p->min_size + 2;
 }
 
-SEQCDC_API int seqcdc_range_chunk_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
-                                       uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
-                                       uint64_t *d_ncuts, uint32_t tail_max, uint64_t *d_tail, uint64_t *d_tail_n,
-                                       uint64_t *d_summary, void *d_ws, size_t ws_bytes, void *stream)
+static int range_chunk_tail_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                                 uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
+                                 uint64_t *d_ncuts, uint32_t tail_max, uint64_t *d_tail, uint64_t *d_tail_n,
+                                 uint64_t *d_summary, void *d_ws, size_t ws_bytes, void *stream, uint64_t *push_blk,
+                                 uint64_t *push_flag, uint64_t push_value)
 {
     if (seqcdc_validate_params(p)) return SEQCDC_EINVAL;
     if (!d_ncuts || range_len > buf_len || entry > range_len) return SEQCDC_EINVAL;
     if (tail_max && (!d_tail || !d_tail_n)) return SEQCDC_EINVAL;
+    if (push_blk && (!push_flag || !d_summary)) return SEQCDC_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     if (entry >= range_len) {
         if (cudaMemsetAsync(d_ncuts, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
         if (tail_max && cudaMemsetAsync(d_tail_n, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
         if (d_summary) k_set2<<<1, 1, 0, st>>>(d_summary, global_offset + entry, 0);
+        if (push_blk) k_push_empty<<<1, 1, 0, st>>>(push_blk, push_flag, global_offset + entry, push_value);
         return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
     }
     if (!d_buf || !d_cuts) return SEQCDC_EINVAL;
@@ -1393,8 +1429,73 @@ SEQCDC_API int seqcdc_range_chunk_tail(const uint8_t *d_buf, uint64_t buf_len, u
     t.tail_n = d_tail_n;
     t.max = tail_max;
     t.summary = d_summary;
+    t.push_blk = push_blk;
+    t.push_flag = push_flag;
+    t.push_value = push_value;
     return enqueue(d_buf + entry, nullptr, 1, buf_len - entry, range_len - entry, global_offset + entry, p, d_cuts,
                    nullptr, d_ncuts, d_ws, ws_bytes, st, true, t);
+}
+
+SEQCDC_API int seqcdc_range_chunk_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,
+                                       uint64_t global_offset, const seqcdc_params_t *p, uint64_t *d_cuts,
+                                       uint64_t *d_ncuts, uint32_t tail_max, uint64_t *d_tail, uint64_t *d_tail_n,
+                                       uint64_t *d_summary, void *d_ws, size_t ws_bytes, void *stream)
+{
+    return range_chunk_tail_impl(d_buf, buf_len, range_len, entry, global_offset, p, d_cuts, d_ncuts, tail_max,
+                                 d_tail, d_tail_n, d_summary, d_ws, ws_bytes, stream, nullptr, nullptr, 0);
+}
+
+SEQCDC_API int seqcdc_range_chunk_tail_push(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
+                                            uint64_t entry, uint64_t global_offset, const seqcdc_params_t *p,
+                                            uint64_t *d_cuts, uint64_t *d_ncuts, uint32_t tail_max, uint64_t *d_tail,
+                                            uint64_t *d_tail_n, uint64_t *d_summary, void *d_ws, size_t ws_bytes,
+                                            uint64_t *d_peer_blk, uint64_t *d_peer_flag, uint64_t flag_value,
+                                            void *stream)
+{
+    if (!d_peer_blk || !d_peer_flag) return SEQCDC_EINVAL;
+    return range_chunk_tail_impl(d_buf, buf_len, range_len, entry, global_offset, p, d_cuts, d_ncuts, tail_max,
+                                 d_tail, d_tail_n, d_summary, d_ws, ws_bytes, stream, d_peer_blk, d_peer_flag,
+                                 flag_value);
+}
+
+// ------------------------------------------------------------------ peer-memory mailboxes (CUDA IPC)
+SEQCDC_API int seqcdc_xchg_alloc(size_t bytes, void **d_buf, void *ipc_handle)
+{
+    if (!d_buf || !ipc_handle || !bytes) return SEQCDC_EINVAL;
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return SEQCDC_ENOMEM;
+    cudaIpcMemHandle_t h;
+    if (cudaMemset(p, 0, bytes) != cudaSuccess || cudaIpcGetMemHandle(&h, p) != cudaSuccess) {
+        cudaFree(p);
+        return SEQCDC_ECUDA;
+    }
+    memcpy(ipc_handle, &h, sizeof(h));
+    *d_buf = p;
+    return SEQCDC_OK;
+}
+
+SEQCDC_API int seqcdc_xchg_open(const void *ipc_handle, void **d_peer)
+{
+    if (!ipc_handle || !d_peer) return SEQCDC_EINVAL;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    void *p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        return SEQCDC_ECUDA;
+    }
+    *d_peer = p;
+    return SEQCDC_OK;
+}
+
+SEQCDC_API int seqcdc_xchg_close(void *d_peer)
+{
+    return (d_peer && cudaIpcCloseMemHandle(d_peer) == cudaSuccess) ? SEQCDC_OK : SEQCDC_ECUDA;
+}
+
+SEQCDC_API int seqcdc_xchg_free(void *d_buf)
+{
+    return (d_buf && cudaFree(d_buf) == cudaSuccess) ? SEQCDC_OK : SEQCDC_ECUDA;
 }
 
 SEQCDC_API int seqcdc_range_chunk(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len, uint64_t entry,

@@ -167,13 +167,52 @@ __global__ void __launch_bounds__(256) k_resync_tail(ResyncArgs a)
 // is also a speculative cut of this range is a merge: the result is e_1..e_i
 // followed by the speculative cuts after it (k_resync_tail).  No merge within
 // the tail (or no tail) leaves status merged = 0 for the re-walk fallback.
-__global__ void __launch_bounds__(128) k_merge_tail(const uint64_t *blk, uint32_t tail_max, ResyncArgs a)
+//
+// Fused-exchange form (wait_flag set): blk is this range's mailbox, filled over
+// peer memory by the previous range's k_post; thread 0 first acquires the flag
+// (system scope) until it reaches wait_value.  After timeout_ns without it the
+// range reports itself empty with overhang ~0 (sum3 then differs from the
+// speculative overhang, so the caller falls back to the collective protocol).
+__global__ void __launch_bounds__(128) k_merge_tail(const uint64_t *blk, uint32_t tail_max, ResyncArgs a,
+                                                    const uint64_t *wait_flag, uint64_t wait_value,
+                                                    uint64_t timeout_ns)
 {
     __shared__ unsigned long long best;                  // (i << 32) | j of the first merge
-    const uint64_t n = min(blk[2], (uint64_t)tail_max);
+    __shared__ int timed_out;
+    if (wait_flag) {
+        if (threadIdx.x == 0) {
+            uint64_t t0, t, v;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            int to = 0;
+#pragma unroll 1
+            for (;;) {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(wait_flag) : "memory");
+                if (v >= wait_value) break;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > timeout_ns) {
+                    to = 1;
+                    break;
+                }
+                __nanosleep(500);
+            }
+            timed_out = to;
+        }
+        __syncthreads();
+        if (timed_out) {
+            if (threadIdx.x == 0) {
+                *a.ncuts = 0;
+                a.status[ST_MERGED] = 2;
+                a.status[ST_M] = 0;
+                a.status[ST_J] = 0;
+                a.status[ST_OVERHANG] = ~0ull;
+            }
+            return;
+        }
+    }
+    const uint64_t n = min(__ldcg(blk + 2), (uint64_t)tail_max);
     const uint64_t *e = blk + 3;
     const uint64_t k = *a.spec_n;
-    const uint64_t ov = blk[0];
+    const uint64_t ov = __ldcg(blk);
     if (threadIdx.x == 0) best = ~0ull;
     __syncthreads();
     if (ov >= a.gofs + a.stop) {                         // no chunk starts in this range
@@ -187,7 +226,7 @@ __global__ void __launch_bounds__(128) k_merge_tail(const uint64_t *blk, uint32_
         return;
     }
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint64_t x = e[i];
+        const uint64_t x = __ldcg(e + i);
         uint64_t lo = 0, hi = k;                         // binary search in the ascending spec list
         while (lo < hi) {
             const uint64_t mid = (lo + hi) >> 1;
@@ -202,7 +241,7 @@ __global__ void __launch_bounds__(128) k_merge_tail(const uint64_t *blk, uint32_
         return;
     }
     const uint64_t im = b >> 32, jm = b & 0xffffffffull;
-    for (uint64_t t = threadIdx.x; t < im; t += blockDim.x) a.out[t] = e[t + 1];
+    for (uint64_t t = threadIdx.x; t < im; t += blockDim.x) a.out[t] = __ldcg(e + t + 1);
     if (threadIdx.x == 0) {
         a.status[ST_MERGED] = 1;
         a.status[ST_M] = im;
@@ -247,6 +286,8 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
                        uint32_t tail_max = 0);
 static thread_local uint64_t *g_sum3 = nullptr;          // merge_tail's optional summary outputs
 static thread_local const uint64_t *g_spec_ov = nullptr;
+static thread_local const uint64_t *g_wait_flag = nullptr; // merge_tail_wait: mailbox flag, value, timeout
+static thread_local uint64_t g_wait_value = 0, g_wait_timeout = 0;
 
 SEQCDC_API int seqcdc_range_merge_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
                                        uint64_t global_offset, const seqcdc_params_t *p, const uint64_t *d_prev,
@@ -261,6 +302,25 @@ SEQCDC_API int seqcdc_range_merge_tail(const uint8_t *d_buf, uint64_t buf_len, u
                                d_ncuts, d_status, stream, d_prev, tail_max);
     g_sum3 = nullptr;
     g_spec_ov = nullptr;
+    return rc;
+}
+
+SEQCDC_API int seqcdc_range_merge_tail_wait(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_len,
+                                            uint64_t global_offset, const seqcdc_params_t *p,
+                                            const uint64_t *d_mailbox, uint32_t tail_max, const uint64_t *d_spec,
+                                            const uint64_t *d_spec_n, uint64_t *d_cuts, uint64_t *d_ncuts,
+                                            uint64_t *d_status, const uint64_t *d_spec_ov, uint64_t *d_sum3,
+                                            const uint64_t *d_flag, uint64_t flag_value, uint64_t timeout_ns,
+                                            void *stream)
+{
+    if (!d_flag) return SEQCDC_EINVAL;
+    g_wait_flag = d_flag;
+    g_wait_value = flag_value;
+    g_wait_timeout = timeout_ns;
+    const int rc = seqcdc_range_merge_tail(d_buf, buf_len, range_len, global_offset, p, d_mailbox, tail_max, d_spec,
+                                           d_spec_n, d_cuts, d_ncuts, d_status, d_spec_ov, d_sum3, stream);
+    g_wait_flag = nullptr;
+    g_wait_value = g_wait_timeout = 0;
     return rc;
 }
 
@@ -320,7 +380,7 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
     a.p.mnL = (uint32_t)p->min_size - p->seq_length;
     seqcdc_ring_geometry(p, &a.p.bs, &a.p.nb, &a.p.ah);
     if (merge_blk) {              // local merge first; the re-walk runs only if it found none
-        k_merge_tail<<<1, 128, 0, st>>>(merge_blk, tail_max, a);
+        k_merge_tail<<<1, 128, 0, st>>>(merge_blk, tail_max, a, g_wait_flag, g_wait_value, g_wait_timeout);
         a.skip = d_status;
     }
     const int ms = a.p.M == 4 ? 4 : (a.p.M < 4 ? 0 : -1);

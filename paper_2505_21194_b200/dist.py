@@ -108,7 +108,9 @@ def chunk_sharded(shard: Shard, backend, group=None, comm_device=None) -> ShardR
     if getattr(backend, "device_protocol", False) and getattr(dev, "type", str(dev)) != "cpu":
         done = _device_round(shard, backend, group, P, r)
         if done is not None:
+            backend.last_path = "p2p" if getattr(backend, "p2p", False) else "device"
             return done
+    backend.last_path = "host"
     spec = backend.spec(shard)
     info = _allgather_i64([spec.overhang, spec.count], group, dev)
     return _host_rounds(shard, backend, group, dev, P, r, spec, info, spec, shard.global_offset, 0, 0)
@@ -126,9 +128,16 @@ def _device_round(shard, backend, group, P, r):
     a re-walk only if the tail is too short).  A second all_gather of
     (overhang, count, speculative overhang) gives the global prefix and proves
     no overhang changed."""
-    spec = backend.spec_dev_tail(shard, last=(r == P - 1))   # extra: "block" [3 + E]
-    blocks = _allgather_dev(spec.extra["block"], group)     # [P, 3 + E]
-    cur = backend.merge_dev(shard, blocks[r - 1], spec) if r > 0 else spec
+    if getattr(backend, "p2p", False):
+        # fused exchange: rank r-1's last kernel stores its block straight into this
+        # rank's mailbox over peer memory; the merge kernel waits for it on the device
+        step = backend.next_step()
+        spec = backend.spec_dev_tail(shard, last=(r == P - 1), push_step=step)
+        cur = backend.merge_dev_wait(shard, spec, step) if r > 0 else spec
+    else:
+        spec = backend.spec_dev_tail(shard, last=(r == P - 1))   # extra: "block" [3 + E]
+        blocks = _allgather_dev(spec.extra["block"], group)     # [P, 3 + E]
+        cur = backend.merge_dev(shard, blocks[r - 1], spec) if r > 0 else spec
     s3 = cur.extra["sum3"] if r > 0 else spec.extra["block"][[0, 1, 0]]   # rank 0's chain is final
     info = _allgather_dev(s3, group)                        # [P, 3] = final ov, count, speculative ov
     h = info.reshape(-1).cpu().tolist()
@@ -174,6 +183,58 @@ class CudaRangeBackend:
         self.stream = stream
         self.device_protocol = True      # spec_dev / resync_dev: no host sync inside a round
         self._key = None
+        self.p2p = False                 # fused exchange over peer memory (enable_p2p)
+        self._mb = self._peer = None
+        self._step = 0
+
+    # ---- fused exchange over peer memory (SURVEY.md 8(e) "fused alternative")
+    def enable_p2p(self, group=None) -> None:
+        """Give this rank a device mailbox (CUDA IPC) and map the next rank's, so
+        the exchange block travels by peer stores from inside rank r's last kernel
+        to rank r+1 (NVLink between GPUs), with a device-side flag instead of the
+        first all_gather.  Collective: every rank calls it once."""
+        from . import xchg_alloc, xchg_open
+        P, r = dist.get_world_size(group), dist.get_rank(group)
+        if P < 2:
+            return False
+        self._flag_off = ((8 * (3 + self.TAIL) + 127) // 128) * 128
+        err = ""
+        with torch.cuda.device(self.device):
+            try:
+                self._mb, h = xchg_alloc(self._flag_off + 128)
+            except Exception as e:       # noqa: BLE001 -- reported to every rank below
+                h, err = b"", f"alloc: {e}"
+            handles = [None] * P
+            dist.all_gather_object(handles, h, group=group)
+            if not err and r + 1 < P and handles[r + 1]:
+                try:
+                    self._peer = xchg_open(handles[r + 1])
+                except Exception as e:   # noqa: BLE001
+                    err = f"open: {e}"
+        # every rank must agree, or the ranks would run different exchanges
+        errs = [None] * P
+        dist.all_gather_object(errs, err, group=group)
+        self._step = 0
+        self.p2p = not any(errs)
+        if not self.p2p:
+            self.close()
+            self.p2p_error = next(e for e in errs if e)
+        return self.p2p
+
+    def next_step(self) -> int:
+        self._step += 1
+        return self._step
+
+    def close(self) -> None:
+        """Unmap the peer mailbox and free this rank's (after all ranks are done)."""
+        from . import xchg_close, xchg_free
+        if self._peer is not None:
+            xchg_close(self._peer)
+            self._peer = None
+        if self._mb is not None:
+            xchg_free(self._mb)
+            self._mb = None
+        self.p2p = False
 
     def _alloc(self, shard: Shard):
         from . import range_max_cuts, workspace_size
@@ -252,15 +313,20 @@ class CudaRangeBackend:
         return Chain(self.out_cuts, -1, -1, {"sum": sm})
 
     # ---- one-exchange device protocol (tails)
-    def spec_dev_tail(self, shard: Shard, last: bool) -> Chain:
-        from . import range_chunk_tail_into
+    def spec_dev_tail(self, shard: Shard, last: bool, push_step: int = 0) -> Chain:
+        from . import range_chunk_tail_into, range_chunk_tail_push_into
         self._alloc(shard)
         E = 0 if last else self.TAIL
         with torch.cuda.device(self.device):
             if last:
                 self.block[2].zero_()
-            range_chunk_tail_into(shard.buf, shard.range_len, shard.global_offset, self.p, self.spec_cuts,
-                                  self.spec_n, E, self.block, workspace=self.ws, stream=self.stream)
+            if push_step and not last:
+                range_chunk_tail_push_into(shard.buf, shard.range_len, shard.global_offset, self.p, self.spec_cuts,
+                                           self.spec_n, E, self.block, self._peer, self._peer + self._flag_off,
+                                           push_step, workspace=self.ws, stream=self.stream)
+            else:
+                range_chunk_tail_into(shard.buf, shard.range_len, shard.global_offset, self.p, self.spec_cuts,
+                                      self.spec_n, E, self.block, workspace=self.ws, stream=self.stream)
         # exchange block = (overhang, count, tail_n, tail); the second exchange
         # for rank 0 is (overhang, count, overhang): its chain is final already
         return Chain(self.spec_cuts, -1, -1, {"block": self.block})
@@ -273,6 +339,16 @@ class CudaRangeBackend:
             range_merge_tail_into(shard.buf, shard.range_len, shard.global_offset, self.p, pb, self.TAIL, spec.cuts,
                                   self.spec_n, self.out_cuts, self.out_n, self.status, spec_ov=self.block,
                                   sum3=self.sum3, stream=self.stream)
+        return Chain(self.out_cuts, -1, -1, {"sum3": self.sum3})
+
+    def merge_dev_wait(self, shard: Shard, spec: Chain, step: int, timeout_ns: int = 2_000_000_000) -> Chain:
+        from . import range_merge_tail_wait_into
+        self._alloc(shard)
+        with torch.cuda.device(self.device):
+            range_merge_tail_wait_into(shard.buf, shard.range_len, shard.global_offset, self.p, self._mb,
+                                       self._mb + self._flag_off, step, self.TAIL, spec.cuts, self.spec_n,
+                                       self.out_cuts, self.out_n, self.status, spec_ov=self.block, sum3=self.sum3,
+                                       timeout_ns=timeout_ns, stream=self.stream)
         return Chain(self.out_cuts, -1, -1, {"sum3": self.sum3})
 
 

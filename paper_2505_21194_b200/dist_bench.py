@@ -45,6 +45,13 @@ def run(args, metric, workload, cfg):
         shard = Shard(buf, hi - lo, lo)
         be = CudaRangeBackend(p, device=dev)
         be.comm_device = cdev
+        # SEQCDC_EXCHANGE=p2p (default): fused exchange over peer memory (the range's
+        # last kernel stores its block into the next rank's mailbox); "collective":
+        # NCCL/gloo all_gather of the blocks
+        exchange = os.environ.get("SEQCDC_EXCHANGE", "p2p")
+        if exchange == "p2p" and world > 1 and not be.enable_p2p():
+            exchange = f"collective (p2p unavailable: {be.p2p_error})"
+        exchange = exchange if world > 1 else "none"
         stream = torch.cuda.current_stream(dev)
         torch.cuda.synchronize()
         for _ in range(args.warmup):
@@ -111,7 +118,8 @@ def run(args, metric, workload, cfg):
                 "vs_baseline": None, "dtype": "u8", "data": "synthetic",
                 "config": {"workload": workload + f"; one stream of {world} x {n_per} bytes, contiguous ranges",
                            "stream_bytes": n, "bytes_per_gpu": n_per,
-                           "parallelism": f"{world} contiguous ranges + NCCL seam exchange (dist.py)",
+                           "parallelism": f"{world} contiguous ranges + seam exchange (dist.py)",
+                           "exchange": exchange, "last_round": getattr(be, "last_path", None),
                            "l2": "input per GPU > 126 MB L2: no flush needed", "ncuts": res.total,
                            "resync_rounds": res.rounds, "dist_backend": backend},
                 "roofline": {"bound": "hbm", "achieved": round(n_per / (walk_ms / 1e3) / 1e9, 1), "peak": peak,
@@ -127,6 +135,8 @@ def run(args, metric, workload, cfg):
                 "parity": {"vs_oracle": "every rank's whole cut list (oracle from its true entry)", "bit_exact": exact},
             }
             print(json.dumps(line), flush=True)
+        dist.barrier()                     # no rank still uses a peer mailbox
+        be.close()
         return 0 if exact else 3
     finally:
         dist.destroy_process_group()

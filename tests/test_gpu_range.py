@@ -107,12 +107,18 @@ def _worker(rank, P, port, kind, seed, n, pidx, q, comm="cpu"):
         else:
             synth.fill_device(kind, seed, lo, buf)
         be = CudaRangeBackend(p)
+        if comm == "p2p":                  # fused exchange: peer-memory mailboxes (CUDA IPC)
+            be.enable_p2p()
+            comm = "cuda"
         cd = torch.device(comm)
         res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=cd)
-        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=cd)   # buffers reused
+        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=cd)   # buffers (and mailboxes) reused
+        path = be.last_path
         cuts = res.cuts[: res.count].cpu().numpy().tolist()
         allc = [None] * P
-        dist.all_gather_object(allc, (rank, res.first_index, res.total, res.rounds, cuts))
+        dist.all_gather_object(allc, (rank, res.first_index, res.total, res.rounds, cuts, path))
+        dist.barrier()
+        be.close()
         if rank == 0:
             q.put(allc)
     finally:
@@ -127,11 +133,17 @@ SHARD_PARAMS = [oracle.table1(8), oracle.table1(4, 1), oracle.table1(16)]
                                                       (4, "uniform", 43, 30 << 20, 2, "cpu"),
                                                       (3, "zeros", 0, 5 << 20, 0, "cpu"),
                                                       (3, "markov", 44, 20 << 20, 1, "cuda"),
-                                                      (4, "zeros", 0, 5 << 20, 0, "cuda")])
+                                                      (4, "zeros", 0, 5 << 20, 0, "cuda"),
+                                                      (2, "markov", 45, 16 << 20, 1, "p2p"),
+                                                      (3, "rampmix", 46, 24 << 20, 0, "p2p"),
+                                                      (3, "zeros", 0, 5 << 20, 0, "p2p")])
 def test_sharded_protocol_on_one_gpu(P, kind, seed, n, pidx, comm):
     """comm="cuda": the device protocol (no host sync inside the round; the
     exchanges run on device tensors), falling back to the host loop on the
-    phase-locked stream."""
+    phase-locked stream.  comm="p2p": the fused exchange -- each range's last
+    kernel stores its block into the next rank's mailbox (CUDA IPC) and the
+    merge kernel waits for the flag on the device; here the ranks share one
+    GPU, across GPUs the stores go over NVLink."""
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -146,10 +158,12 @@ def test_sharded_protocol_on_one_gpu(P, kind, seed, n, pidx, comm):
     b = np.zeros(n, np.uint8) if kind == "zeros" else synth.fill_host(kind, seed, 0, n)
     want = oracle.chunk(b, SHARD_PARAMS[pidx])
     got = []
-    for rank, first, total, rounds, cuts in sorted(allc):
+    for rank, first, total, rounds, cuts, path in sorted(allc):
         assert first == len(got)
         got += cuts
         assert total == want.size
+        if comm == "p2p" and kind != "zeros":   # the fused round settled it (no fallback)
+            assert path == "p2p", (rank, path)
     assert np.array_equal(np.asarray(got, np.uint64), want)
 
 
@@ -256,3 +270,57 @@ def test_batch_sharded_lpt(P):
         want_total += w.size
         assert np.array_equal(np.asarray(got[j], np.uint64), w), j
     assert all(t == want_total for _, t in allr)
+
+
+def test_fused_push_and_wait_single_process():
+    """The fused-exchange pieces in one process: seqcdc_range_chunk_tail_push
+    stores the block into the given mailbox address and releases the flag;
+    seqcdc_range_merge_tail_wait on that mailbox gives the next range's true
+    chain (= the oracle), exactly as seqcdc_range_merge_tail on the block; with a
+    flag value that never arrives it times out into the collective-fallback
+    signal (overhang UINT64_MAX) instead of hanging."""
+    p = oracle.table1(8)
+    sp = _sp(p)
+    n = 8 << 20
+    b = synth.fill_host("markov", 61, 0, n)
+    full = oracle.chunk(b, p)
+    E, R1 = 96, 3 << 20
+    end0 = R1 + (E + 1) * p.max_size
+    buf0 = torch.from_numpy(b[:end0]).cuda()
+    cap0 = sc.range_max_cuts(buf0.numel(), R1, sp)
+    c0 = torch.empty(cap0, dtype=torch.int64, device="cuda")
+    n0 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    blk = torch.zeros(3 + E, dtype=torch.int64, device="cuda")
+    mb, handle = sc.xchg_alloc(4096)
+    try:
+        assert len(handle) == sc.IPC_HANDLE_BYTES
+        flag = mb + 2048
+        sc.range_chunk_tail_push_into(buf0, R1, 0, sp, c0, n0, E, blk, mb, flag, 7)
+        k0 = int(n0.item())
+        ov = int(c0[k0 - 1].item())
+        assert blk[:2].cpu().tolist() == [ov, k0]
+        # the next range: its speculative chain, then the merge from the mailbox
+        buf1 = torch.from_numpy(b[R1:]).cuda()
+        cap1 = sc.range_max_cuts(buf1.numel(), n - R1, sp)
+        spec = torch.empty(cap1, dtype=torch.int64, device="cuda")
+        spec_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+        own = torch.zeros(3 + E, dtype=torch.int64, device="cuda")
+        sc.range_chunk_tail_into(buf1, n - R1, R1, sp, spec, spec_n, 0, own)
+        out = torch.empty(cap1, dtype=torch.int64, device="cuda")
+        out_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+        status = torch.zeros(4, dtype=torch.int64, device="cuda")
+        sum3 = torch.zeros(3, dtype=torch.int64, device="cuda")
+        sc.range_merge_tail_wait_into(buf1, n - R1, R1, sp, mb, flag, 7, E, spec, spec_n, out, out_n, status,
+                                      spec_ov=own, sum3=sum3)
+        want = full[full > ov]
+        got = out[: int(out_n.item())].cpu().numpy().astype(np.uint64)
+        assert np.array_equal(got, want)
+        assert sum3.cpu().tolist()[:2] == [int(want[-1]), int(want.size)]
+        # a flag value that never arrives: bounded wait, then the fallback signal
+        sc.range_merge_tail_wait_into(buf1, n - R1, R1, sp, mb, flag, 8, E, spec, spec_n, out, out_n, status,
+                                      spec_ov=own, sum3=sum3, timeout_ns=2_000_000)
+        s3 = sum3.cpu().tolist()
+        assert s3[0] == -1 and s3[1] == 0 and s3[2] == int(own[0].item())
+    finally:
+        torch.cuda.synchronize()
+        sc.xchg_free(mb)
