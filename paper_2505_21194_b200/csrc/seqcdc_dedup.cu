@@ -13,6 +13,7 @@
 // (d_ncuts, e.g. straight from seqcdc_chunk); grids are sized by a host bound.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 
@@ -88,36 +89,18 @@ __device__ __forceinline__ void sha256_block(uint32_t st[8], uint32_t w[16], uin
 // that start before the chunk end, so never past the buffer's last word)
 __device__ __forceinline__ uint32_t ldw(const uint8_t *p) { return __ldg((const uint32_t *)p); }
 
-__global__ void __launch_bounds__(128) k_sha256(const uint8_t *in, const uint64_t *cuts, const uint64_t *ncuts_p,
-                                                uint64_t cap, uint8_t *digests, uint32_t one)
+// Message word j of block k of a chunk [s, e) (FIPS 180-4 §5.1.1 padding):
+// the data bytes of the block, 0x80 right after the last data byte, zeros, and
+// the 64-bit bit length in words 14-15 of the chunk's last block.  Words that
+// start at or past the chunk end are never loaded.
+__device__ __forceinline__ void load_block(uint32_t w[16], const uint8_t *in, uint64_t s, uint64_t e, uint64_t k,
+                                           bool last)
 {
-    const uint64_t ncuts = *ncuts_p;
-    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ncuts || i >= cap) return;
-    const uint64_t s = i ? cuts[i - 1] : 0, e = cuts[i];
     const uint64_t len = e - s;
-    uint32_t st[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
-                      0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
-    uint32_t w[16];
-    const uint64_t nfull = len >> 6;
-    const uintptr_t ab = (uintptr_t)in;
-    for (uint64_t k = 0; k < nfull; k++) {
-        const uintptr_t o = ab + s + 64 * k;
-        const uint8_t *base = (const uint8_t *)(o & ~(uintptr_t)3);
-        const uint32_t sh = 8u * (uint32_t)(o & 3);
-        uint32_t prev = ldw(base);
-#pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const uint32_t nx = (sh || j < 15) ? ldw(base + 4 * (j + 1)) : 0u;
-            w[j] = bswap(__funnelshift_r(prev, nx, sh));
-            prev = nx;
-        }
-        sha256_block(st, w, one);
-    }
-    // final block(s): the remaining rem bytes, 0x80, zeros, 64-bit bit length (FIPS 180-4 §5.1.1)
-    const uint32_t rem = (uint32_t)(len & 63);
-    const uintptr_t o = ab + s + 64 * nfull;
-    const uintptr_t endp = ab + e;
+    const uint64_t rest = len - 64 * k;                     // data bytes from this block on (wraps when past the end)
+    const int32_t valid = 64 * k > len ? -1 : (rest > 64 ? 64 : (int32_t)rest);   // data bytes in this block
+    const uintptr_t o = (uintptr_t)in + s + 64 * k;
+    const uintptr_t endp = (uintptr_t)in + e;
     const uint8_t *base = (const uint8_t *)(o & ~(uintptr_t)3);
     const uint32_t sh = 8u * (uint32_t)(o & 3);
     uint32_t prev = (uintptr_t)base < endp ? ldw(base) : 0u;
@@ -127,28 +110,72 @@ __global__ void __launch_bounds__(128) k_sha256(const uint8_t *in, const uint64_
         const uint32_t nx = (uintptr_t)p < endp ? ldw(p) : 0u;
         uint32_t v = bswap(__funnelshift_r(prev, nx, sh));
         prev = nx;
-        const int valid = (int)rem - 4 * j;                  // message bytes in this word
-        if (valid <= 0) v = 0;
-        else if (valid < 4) v &= ~(0xffffffffu >> (8 * valid));
-        if (valid >= 0 && valid < 4) v |= 0x80u << (24 - 8 * valid);
+        const int32_t vb = valid - 4 * j;                     // message bytes in this word
+        if (vb <= 0) v = 0;
+        else if (vb < 4) v &= ~(0xffffffffu >> (8 * vb));
+        if (vb >= 0 && vb < 4) v |= 0x80u << (24 - 8 * vb);
         w[j] = v;
     }
-    const uint64_t bits = len * 8;
-    if (rem <= 55) {
+    if (last) {
+        const uint64_t bits = len * 8;
         w[14] = (uint32_t)(bits >> 32);
         w[15] = (uint32_t)bits;
-        sha256_block(st, w, one);
-    } else {
-        sha256_block(st, w, one);
-#pragma unroll
-        for (int j = 0; j < 14; j++) w[j] = 0;
-        w[14] = (uint32_t)(bits >> 32);
-        w[15] = (uint32_t)bits;
-        sha256_block(st, w, one);
     }
-    uint4 *out = (uint4 *)(digests + 32 * i);
-    out[0] = make_uint4(bswap(st[0]), bswap(st[1]), bswap(st[2]), bswap(st[3]));
-    out[1] = make_uint4(bswap(st[4]), bswap(st[5]), bswap(st[6]), bswap(st[7]));
+}
+
+// Persistent, load-balanced: every lane compresses one 64-byte block per
+// iteration (data or padding, the same straight-line code), so the 64-round
+// compression never diverges; a lane that finishes its chunk writes the digest
+// and takes the next chunk index from a counter (one atomic per warp), so the
+// lanes of a warp no longer wait for the longest of 32 fixed chunks.
+// (Prefetching the next chunk's bounds one chunk ahead measured slower:
+// profiles/r01/dedup_next1_v3.jsonl.)
+__global__ void __launch_bounds__(128) k_sha256(const uint8_t *in, const uint64_t *cuts, const uint64_t *ncuts_p,
+                                                uint64_t cap, uint8_t *digests, uint32_t one,
+                                                unsigned long long *next)
+{
+    const uint64_t n = min(*ncuts_p, cap);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t T = (uint64_t)gridDim.x * blockDim.x;    // the first T chunks are assigned statically
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool act = i < n;
+    uint64_t s = 0, e = 0, k = 0, nblk = 0;
+    uint32_t st[8];
+    auto start = [&]() {
+        s = i ? cuts[i - 1] : 0;
+        e = cuts[i];
+        const uint64_t len = e - s;
+        nblk = (len >> 6) + ((len & 63) <= 55 ? 1 : 2);
+        k = 0;
+        st[0] = 0x6a09e667u; st[1] = 0xbb67ae85u; st[2] = 0x3c6ef372u; st[3] = 0xa54ff53au;
+        st[4] = 0x510e527fu; st[5] = 0x9b05688cu; st[6] = 0x1f83d9abu; st[7] = 0x5be0cd19u;
+    };
+    if (act) start();
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll 1
+    while (__any_sync(0xffffffffu, act)) {
+        uint32_t w[16];
+        load_block(w, in, act ? s : 0, act ? e : 0, k, act && k + 1 == nblk);
+        sha256_block(st, w, one);
+        const bool fin = act && ++k == nblk;
+        if (fin) {
+            uint4 *out = (uint4 *)(digests + 32 * i);
+            out[0] = make_uint4(bswap(st[0]), bswap(st[1]), bswap(st[2]), bswap(st[3]));
+            out[1] = make_uint4(bswap(st[4]), bswap(st[5]), bswap(st[6]), bswap(st[7]));
+        }
+        const uint32_t want = __ballot_sync(0xffffffffu, fin);
+        if (want) {
+            const int leader = __ffs(want) - 1;
+            unsigned long long b = 0;
+            if ((int)lane == leader) b = atomicAdd(next, (unsigned long long)__popc(want));
+            b = __shfl_sync(0xffffffffu, b, leader);
+            if (fin) {
+                i = T + b + __popc(want & lt);
+                act = i < n;
+                if (act) start();
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------- dedup index
@@ -242,9 +269,21 @@ SEQCDC_API int seqcdc_fingerprint(const uint8_t *d_in, const uint64_t *d_cuts, c
     if (!d_ncuts || (max_cuts && (!d_in || !d_cuts || !d_digests))) return SEQCDC_EINVAL;
     if (((uintptr_t)d_digests & 15) != 0) return SEQCDC_EINVAL;
     if (max_cuts == 0) return SEQCDC_OK;
-    const uint64_t grid = (max_cuts + 127) / 128;
-    if (grid > 0x7fffffffu) return SEQCDC_EINVAL;
-    k_sha256<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(d_in, d_cuts, d_ncuts, max_cuts, d_digests, 1u);
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // persistent grid: exactly the resident CTAs (all of them start at once, so the
+    // statically assigned first chunks do not wait for a second wave), never more
+    // threads than chunks
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sha256, 128, 0) != cudaSuccess || occ < 1) occ = 4;
+    const uint64_t grid = std::min<uint64_t>((max_cuts + 127) / 128, (uint64_t)sms * occ);
+    unsigned long long *next = nullptr;               // chunk counter for the dynamic assignment
+    if (cudaMallocAsync((void **)&next, 8, st) != cudaSuccess) return SEQCDC_ENOMEM;
+    cudaMemsetAsync(next, 0, 8, st);
+    k_sha256<<<(unsigned)grid, 128, 0, st>>>(d_in, d_cuts, d_ncuts, max_cuts, d_digests, 1u, next);
+    cudaFreeAsync(next, st);
     return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
 }
 
