@@ -1299,6 +1299,10 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
 
 using namespace seqcdc;
 
+// the library's stream-ordered pool (no trimming at synchronisation), for the
+// other translation units' small per-call allocations
+int seqcdc_internal_pool(cudaMemPool_t *pool) { return get_pool(*pool); }
+
 // internal, used by seqcdc_range.cu (hidden visibility: not part of the ABI)
 void seqcdc_ring_geometry(const seqcdc_params_t *p, uint32_t *bs, uint32_t *nb, uint32_t *ah)
 {

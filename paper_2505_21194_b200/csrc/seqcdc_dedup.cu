@@ -15,11 +15,14 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/seqcdc.h"
 
 #define SEQCDC_API extern "C" __attribute__((visibility("default")))
+// internal (seqcdc.cu): the library's memory pool (keeps its memory across syncs)
+int seqcdc_internal_pool(cudaMemPool_t *pool);
 
 namespace seqcdc {
 namespace {
@@ -278,9 +281,12 @@ SEQCDC_API int seqcdc_fingerprint(const uint8_t *d_in, const uint64_t *d_cuts, c
     // threads than chunks
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sha256, 128, 0) != cudaSuccess || occ < 1) occ = 4;
+    if (const char *e = getenv("SEQCDC_SHA_CTAS_PER_SM")) occ = std::max(1, std::min(occ, atoi(e)));   // tuning
     const uint64_t grid = std::min<uint64_t>((max_cuts + 127) / 128, (uint64_t)sms * occ);
     unsigned long long *next = nullptr;               // chunk counter for the dynamic assignment
-    if (cudaMallocAsync((void **)&next, 8, st) != cudaSuccess) return SEQCDC_ENOMEM;
+    cudaMemPool_t pool;
+    if (seqcdc_internal_pool(&pool) != SEQCDC_OK) return SEQCDC_ECUDA;
+    if (cudaMallocFromPoolAsync((void **)&next, 8, pool, st) != cudaSuccess) return SEQCDC_ENOMEM;
     cudaMemsetAsync(next, 0, 8, st);
     k_sha256<<<(unsigned)grid, 128, 0, st>>>(d_in, d_cuts, d_ncuts, max_cuts, d_digests, 1u, next);
     cudaFreeAsync(next, st);
@@ -302,7 +308,9 @@ SEQCDC_API int seqcdc_dedup(const uint8_t *d_digests, const uint64_t *d_cuts, co
     if (table) {
         if (ws_bytes < 8 * cap) return SEQCDC_ENOMEM;
     } else {
-        if (cudaMallocAsync((void **)&table, 8 * cap, st) != cudaSuccess) return SEQCDC_ENOMEM;
+        cudaMemPool_t pool;
+        if (seqcdc_internal_pool(&pool) != SEQCDC_OK) return SEQCDC_ECUDA;
+        if (cudaMallocFromPoolAsync((void **)&table, 8 * cap, pool, st) != cudaSuccess) return SEQCDC_ENOMEM;
         owned = true;
     }
     k_dedup_clear<<<592, 256, 0, st>>>(table, cap, d_unique_bytes);
