@@ -18,7 +18,8 @@ import paper_2505_21194_b200 as sc  # noqa: E402
 
 
 def _sp(p):
-    return sc.SeqParams(p.mode, p.seq_length, p.skip_trigger, p.skip_size, p.min_size, p.max_size)
+    return sc.SeqParams(p.mode, p.seq_length, p.skip_trigger, p.skip_size, p.min_size, p.max_size,
+                        (sc.FLAG_SIGNED if p.signed else 0) | (sc.FLAG_PAIRS if p.pairs else 0))
 
 
 def _oracle_chain(buf, start, range_len, gofs, p):
@@ -31,7 +32,9 @@ def _oracle_chain(buf, start, range_len, gofs, p):
 
 
 CASES = [("uniform", 31, oracle.table1(8)), ("markov", 32, oracle.table1(4, 1)), ("rampmix", 33, oracle.table1(8)),
-         ("zeroheavy", 34, oracle.table1(16))]
+         ("zeroheavy", 34, oracle.table1(16)),
+         # the reading flags go through the range calls too
+         ("uniform", 35, oracle.Params(0, 4, 50, 256, 4096, 16384, signed=True, pairs=True))]
 
 
 @pytest.mark.parametrize("kind,seed,p", CASES)
