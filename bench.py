@@ -21,7 +21,6 @@ import argparse
 import json
 import os
 import platform
-import subprocess
 import sys
 import threading
 import time

@@ -1,7 +1,6 @@
 """CPU-only checks of the C ABI boundary: libseqcdc.so builds for sm_100a,
 loads without a GPU, exports every function include/*.h declares, and its
 host-side parameter logic behaves as documented.  No compute calls."""
-import ctypes
 import glob
 import os
 import re
