@@ -259,10 +259,11 @@ __device__ __forceinline__ void tl_mark(uint32_t s, int k)
     if (g_tl && s < g_tl_cap && threadIdx.x == 0) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        uint32_t smid;
+        uint32_t smid, wid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
         g_tl[4 * s + k] = t;
-        g_tl[4 * s + 3] = smid;
+        g_tl[4 * s + 3] = smid | ((uint64_t)wid << 32);
     }
 }
 #define TL_MARK(s, k) tl_mark((s), (k))
