@@ -356,7 +356,11 @@ __device__ int check_cut(const Work &w, Cursor &c, uint32_t t, uint64_t t_lo, ui
     }
 }
 
-template <int MODE, int MSPEC>
+// BR: the decision used for the speculative bulk (resolve's RED).  Measured:
+// the warp min-reduction is faster on single streams (config 2 +3%, 4 GiB
+// Markov +3%), the ballot decision on batches of mixed streams (config 3 4 KiB
+// row +6%, 8 KiB +2%); extensions and re-walks always use the min-reduction.
+template <int MODE, int MSPEC, bool BR>
 __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
 {
     TL_MARK(s, 0);
@@ -377,7 +381,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
     // spec phase: cuts < hi belong to L_s
 #pragma unroll 1
     while (base < end_rel) {
-        c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+        c = resolve<MODE, MSPEC, BR>(wk, w.p, base, lane);
         if (c >= hi_rel) {
             extend = true;
             break;
@@ -572,7 +576,7 @@ __device__ void fix_overflows(const Work &w, Walker &wk, int lane)
     }
 }
 
-template <int MODE, int MSPEC>
+template <int MODE, int MSPEC, bool BR>
 __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
 {
     __shared__ __align__(128) uint8_t ring[RING];
@@ -587,7 +591,7 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
         if (lane == 0) s = atomicAdd(w.ctrl + C_NEXT, 1u);
         s = __shfl_sync(FULL, s, 0);
         if (s >= nseg) break;
-        walk_segment<MODE, MSPEC>(w, wk, s, lane);
+        walk_segment<MODE, MSPEC, BR>(w, wk, s, lane);
     }
     if (w.single) {
         // the last walker to finish continues any extension on the valid path
@@ -995,7 +999,7 @@ static int device_info(int &sms, int &occ, uint32_t smem = 0)
     const uint32_t key = std::min<uint32_t>(smem / 1024, 65);
     if (!g_occ_by_smem[key]) {
         int occ_ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4>, 32, smem) != cudaSuccess)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4, true>, 32, smem) != cudaSuccess)
             return SEQCDC_ECUDA;
         // 24 walkers per SM measured best (25 -- the smem limit -- leaves almost no L1
         // and runs ~25% slower on config 2; profiles/r01/sweeps.md)
@@ -1123,7 +1127,8 @@ template <int MODE, int MSPEC>
 static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
 {
     prof_mark(pr, 1, st);
-    k_walk<MODE, MSPEC><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
+    if (w.single) k_walk<MODE, MSPEC, true><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
+    else k_walk<MODE, MSPEC, false><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
     prof_mark(pr, 2, st);
     if (w.single) {
         // programmatic dependent launch: k_post's CTAs become resident on SMs the

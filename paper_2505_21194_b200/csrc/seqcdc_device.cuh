@@ -453,9 +453,18 @@ __device__ __forceinline__ uint32_t run_mask(uint32_t Fm, uint32_t carry, uint32
 // neither -> next window.  Pairs and bytes come from the warp's ring.
 // (The min-reduction replaced ballot + ffs + shuffle: lone-walker latency
 // 0.80 -> 0.745 us per chunk, profiles/r01/sweeps.md.)
-template <int MODE, int MSPEC>
+// RED selects how the decision finds the first run end / the T-th opposing
+// pair: true = per-lane candidates + two warp min-reductions (REDUX: shortest
+// dependent chain, used where a walker runs alone, i.e. extensions and
+// re-walks), false = two ballots + __ffs + two shuffles (cheaper in issue
+// slots, used for the speculative bulk, which shares the SM with 21 others).
+#ifndef SEQCDC_DEC_FORCE
+#define SEQCDC_DEC_FORCE -1   // tuning: 0 = ballots everywhere, 1 = REDUX everywhere
+#endif
+template <int MODE, int MSPEC, bool RED_ = true>
 __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint32_t base, int lane)
 {
+    constexpr bool RED = SEQCDC_DEC_FORCE < 0 ? RED_ : SEQCDC_DEC_FORCE == 1;
     uint32_t limit = base + p.mx;                  // P:266 (no overflow: base < 3 GiB, mx <= 2^28)
     if (limit > wk.end_rel) limit = wk.end_rel;
     const uint32_t lim2 = limit - 2;               // last pair that may be examined
@@ -500,15 +509,21 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
         const uint32_t b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),
                        b2 = __ballot_sync(FULL, cnt & 4);
         const uint32_t excl = __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask);
-        // per-lane candidates, the first of each by a warp min-reduction
         constexpr uint32_t NONE = 0xffffffffu;
-        const uint32_t rc = R ? 4 * (uint32_t)lane + ((uint32_t)(__ffs(R) - 1) >> 3) : NONE;
-        const uint32_t pcr = (Om >> 7) * 0x01010101u;
-        const uint32_t ger = ((pcr | H) - (need - excl) * 0x01010101u) & 0x00808080u;
-        const uint32_t dc = (excl < need && excl + cnt >= need) ? 4 * (uint32_t)lane + 3u - __popc(ger) : NONE;
-        const uint32_t r = __reduce_min_sync(FULL, rc);
-        const uint32_t d = __reduce_min_sync(FULL, dc);
-        if ((r & d) == NONE) {                     // nothing decided in this window
+        uint32_t r = NONE, d = NONE, rmask = 0, dmask = 0;
+        if (RED) {
+            // per-lane candidates, the first of each by a warp min-reduction
+            const uint32_t rc = R ? 4 * (uint32_t)lane + ((uint32_t)(__ffs(R) - 1) >> 3) : NONE;
+            const uint32_t pcr = (Om >> 7) * 0x01010101u;
+            const uint32_t ger = ((pcr | H) - (need - excl) * 0x01010101u) & 0x00808080u;
+            const uint32_t dc = (excl < need && excl + cnt >= need) ? 4 * (uint32_t)lane + 3u - __popc(ger) : NONE;
+            r = __reduce_min_sync(FULL, rc);
+            d = __reduce_min_sync(FULL, dc);
+        } else {
+            rmask = __ballot_sync(FULL, R != 0);
+            dmask = __ballot_sync(FULL, excl + cnt >= need);
+        }
+        if (RED ? (r & d) == NONE : (rmask | dmask) == 0) {   // nothing decided in this window
             need -= __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
             carry = MSPEC >= 0 ? __shfl_sync(FULL, Fm, 31) : Fm;
             const bool flat = !__any_sync(FULL, (Fm | Om) != 0);
@@ -538,6 +553,18 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
                 }
             }
             continue;
+        }
+        if (!RED) {
+            // per lane: byte of its first run end, byte of its k-th opposing pair
+            // (k = need - excl; byte j of pc = opposing flags in bytes 0..j)
+            const uint32_t rbyte = (uint32_t)(__ffs(R) - 1) >> 3;
+            const uint32_t pc = (Om >> 7) * 0x01010101u;
+            const uint32_t ge = ((pc | H) - (need - excl) * 0x01010101u) & 0x00808080u;
+            const uint32_t dbyte = 3u - __popc(ge);
+            const uint32_t rl = rmask ? (uint32_t)__ffs(rmask) - 1 : 32u;
+            const uint32_t dl = dmask ? (uint32_t)__ffs(dmask) - 1 : 32u;
+            r = 4 * rl + __shfl_sync(FULL, rbyte, rl & 31);
+            d = 4 * dl + __shfl_sync(FULL, dbyte, dl & 31);
         }
         if (r < d) {                               // the run completes first: boundary after it
             const uint32_t ra = p0 + r;
