@@ -1,0 +1,83 @@
+#!/usr/bin/env python
+"""Randomised parity stress (GPU box): random parameters, data kinds, sizes,
+segment lengths, alignments, flags and call forms (single stream / batch),
+every result compared with the oracle.  Prints one JSON summary line; exits 1
+on the first mismatch (printing the case to reproduce it).
+
+  python tools/stress.py [seconds] [seed]"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2505_21194_b200 as sc  # noqa: E402
+
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 600.0
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+KINDS = ["uniform", "markov", "zeroheavy", "rampmix"]
+
+
+def rand_params():
+    L = int(rng.integers(2, 9))
+    pairs = bool(rng.random() < 0.15)
+    mn = int(rng.choice([L, L + 1, 64, 300, 1024, 2048, 4096, 8192]))
+    mn = max(mn, L)
+    mx = int(mn * rng.choice([1, 1.5, 2, 4, 8])) + int(rng.integers(0, 3))
+    return oracle.Params(int(rng.integers(0, 2)), L, int(rng.integers(1, 120)), int(rng.choice([0, 1, 7, 64, 256, 511, 600])),
+                         mn, mx, signed=bool(rng.random() < 0.15), pairs=pairs)
+
+
+def sp(p):
+    return sc.SeqParams(p.mode, p.seq_length, p.skip_trigger, p.skip_size, p.min_size, p.max_size,
+                        (sc.FLAG_SIGNED if p.signed else 0) | (sc.FLAG_PAIRS if p.pairs else 0))
+
+
+def data(n):
+    k = rng.choice(KINDS + ["alphabet", "const"])
+    if k == "alphabet":
+        return rng.integers(0, int(rng.choice([2, 3, 5])), n).astype(np.uint8), "alphabet"
+    if k == "const":
+        return np.full(n, int(rng.integers(0, 256)), np.uint8), "const"
+    return synth.fill_host(str(k), int(rng.integers(0, 1000)), int(rng.integers(0, 1 << 20)), n), str(k)
+
+
+t0 = time.time()
+cases = cuts_checked = 0
+while time.time() - t0 < budget:
+    p = rand_params()
+    n = int(rng.choice([0, 1, 5, 100, 4096, 100000, 1 << 20, 5 << 20, 24 << 20])) + int(rng.integers(0, 4096))
+    b, kind = data(n)
+    G = int(rng.choice([0, 0, 1 << 14, 1 << 16, 1 << 18]))
+    sc.set_segment_bytes(G)
+    form = "batch" if rng.random() < 0.3 else "single"
+    try:
+        if form == "single":
+            off = int(rng.integers(0, 16))
+            buf = torch.zeros(n + off, dtype=torch.uint8, device="cuda")
+            if n:
+                buf[off:] = torch.from_numpy(b).cuda()
+            got = sc.chunk(buf[off:], sp(p)).cpu().numpy().astype(np.uint64)
+            want = oracle.chunk(b, p)
+        else:
+            ns = int(rng.integers(1, 12))
+            cutsp = np.sort(rng.integers(0, n + 1, ns - 1)) if ns > 1 else np.zeros(0, np.int64)
+            offs = np.concatenate([[0], cutsp, [n]]).astype(np.uint64)
+            gc, gi = sc.chunk_batch(torch.from_numpy(b).cuda() if n else torch.zeros(0, dtype=torch.uint8, device="cuda"),
+                                    torch.from_numpy(offs.astype(np.int64)).cuda(), sp(p))
+            got = np.concatenate([gi.cpu().numpy().astype(np.uint64), gc.cpu().numpy().astype(np.uint64)])
+            wc, wi = oracle.chunk_batch(b, offs, p)
+            want = np.concatenate([wi.astype(np.uint64), wc.astype(np.uint64)])
+    finally:
+        sc.set_segment_bytes(0)
+    cases += 1
+    cuts_checked += int(want.size)
+    if got.shape != want.shape or not np.array_equal(got, want):
+        print(json.dumps({"mismatch": True, "form": form, "kind": kind, "n": n, "G": G, "params": repr(p)}))
+        sys.exit(1)
+print(json.dumps({"stress": "ok", "cases": cases, "cuts_checked": cuts_checked, "seconds": round(time.time() - t0, 1)}))
