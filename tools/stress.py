@@ -47,17 +47,64 @@ def data(n):
     return synth.fill_host(str(k), int(rng.integers(0, 1000)), int(rng.integers(0, 1 << 20)), n), str(k)
 
 
+def range_case(b, n, p):
+    """The multi-GPU seam protocol emulated in one process: P contiguous ranges
+    (each with its halo), speculative pass + tail per range, then in rank order
+    the local merge with the previous range's tail block (when that range's
+    overhang stayed speculative) or a re-walk from the true entry."""
+    E = 96
+    P = int(rng.integers(2, 6))
+    R = sorted(set([0, n] + rng.integers(p.max_size, n - p.max_size, P - 1).tolist()))
+    R = [x for i, x in enumerate(R) if i == 0 or x - R[i - 1] >= p.max_size or x == n]
+    if R[-1] != n:
+        R.append(n)
+    P = len(R) - 1
+    q = sp(p)
+    out, spec_ov, prev_blk, true_ov = [], None, None, None
+    for r in range(P):
+        lo, hi = R[r], R[r + 1]
+        end = n if r == P - 1 else min(n, hi + (E + 1) * p.max_size)
+        buf = torch.from_numpy(b[lo:end]).cuda()
+        cap = sc.range_max_cuts(buf.numel(), hi - lo, q)
+        spec = torch.empty(cap, dtype=torch.int64, device="cuda")
+        spec_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+        blk = torch.zeros(3 + E, dtype=torch.int64, device="cuda")
+        sc.range_chunk_tail_into(buf, hi - lo, lo, q, spec, spec_n, 0 if r == P - 1 else E, blk)
+        if r == 0:
+            cuts = spec[: int(spec_n.item())].cpu().numpy().astype(np.uint64)
+            ov = int(blk[0].item())
+        else:
+            res = torch.empty(cap, dtype=torch.int64, device="cuda")
+            res_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+            status = torch.zeros(4, dtype=torch.int64, device="cuda")
+            if prev_spec_ov == true_ov:        # the previous tail continues the true chain
+                sum3 = torch.zeros(3, dtype=torch.int64, device="cuda")
+                sc.range_merge_tail_into(buf, hi - lo, lo, q, prev_blk, E, spec, spec_n, res, res_n, status,
+                                         spec_ov=blk, sum3=sum3)
+            else:
+                sc.range_resync_into(buf, hi - lo, true_ov - lo, lo, q, spec, spec_n, res, res_n, status)
+            cuts = res[: int(res_n.item())].cpu().numpy().astype(np.uint64)
+            ov = int(status[3].item())
+        out.append(cuts)
+        prev_blk, prev_spec_ov, true_ov = blk, int(blk[0].item()), ov
+    return np.concatenate(out) if out else np.zeros(0, np.uint64), oracle.chunk(b, p)
+
+
 t0 = time.time()
 cases = cuts_checked = 0
+forms = {"single": 0, "batch": 0, "range": 0}
 while time.time() - t0 < budget:
     p = rand_params()
     n = int(rng.choice([0, 1, 5, 100, 4096, 100000, 1 << 20, 5 << 20, 24 << 20])) + int(rng.integers(0, 4096))
     b, kind = data(n)
     G = int(rng.choice([0, 0, 1 << 14, 1 << 16, 1 << 18]))
     sc.set_segment_bytes(G)
-    form = "batch" if rng.random() < 0.3 else "single"
+    u = rng.random()
+    form = "batch" if u < 0.25 else ("range" if u < 0.45 and n >= 8 * p.max_size else "single")
     try:
-        if form == "single":
+        if form == "range":
+            got, want = range_case(b, n, p)
+        elif form == "single":
             off = int(rng.integers(0, 16))
             buf = torch.zeros(n + off, dtype=torch.uint8, device="cuda")
             if n:
@@ -76,8 +123,10 @@ while time.time() - t0 < budget:
     finally:
         sc.set_segment_bytes(0)
     cases += 1
+    forms[form] += 1
     cuts_checked += int(want.size)
     if got.shape != want.shape or not np.array_equal(got, want):
         print(json.dumps({"mismatch": True, "form": form, "kind": kind, "n": n, "G": G, "params": repr(p)}))
         sys.exit(1)
-print(json.dumps({"stress": "ok", "cases": cases, "cuts_checked": cuts_checked, "seconds": round(time.time() - t0, 1)}))
+print(json.dumps({"stress": "ok", "cases": cases, "forms": forms, "cuts_checked": cuts_checked,
+                  "seconds": round(time.time() - t0, 1)}))
