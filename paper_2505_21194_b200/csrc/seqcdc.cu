@@ -1025,7 +1025,14 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     const uint64_t walkers = (uint64_t)sms * occ_eff;
     const uint64_t mx = p->max_size, mn = p->min_size;
     // segments per walker (x100; tuning knob) and the segment floor in max_size units
-    const uint64_t spw = (uint64_t)std::max(1, env_int("SEQCDC_SEGS_PER_WALKER_X100", 100));
+    // Batches of streams: two segments per walker for the 4 and 8 KiB rows (the
+    // second wave is claimed by whichever walkers finish first, which evens out
+    // the warp-slot unfairness: config 3 4 KiB row +15%, 8 KiB +10%); one for
+    // larger rows, whose long merge distances make the extra seams cost more
+    // (16 KiB row -8% at two).  A single stream keeps one: its overflowing
+    // extensions are continued by one warp (profiles/r01/sweeps.md).
+    const int spw_default = (!single && p->min_size <= 4096) ? 200 : 100;
+    const uint64_t spw = (uint64_t)std::max(1, env_int("SEQCDC_SEGS_PER_WALKER_X100", spw_default));
     const uint64_t floor_chunks = (uint64_t)std::max(1, env_int("SEQCDC_G_FLOOR_CHUNKS", (int)G_FLOOR_CHUNKS));
     uint64_t denom = walkers > 2ull * ns ? walkers - ns : std::max<uint64_t>(walkers / 2, 1);
     denom = std::max<uint64_t>(1, denom * spw / 100);
