@@ -198,17 +198,21 @@ class CudaRangeBackend:
         if P < 2:
             return False
         self._flag_off = ((8 * (3 + self.TAIL) + 127) // 128) * 128
-        err = ""
-        with torch.cuda.device(self.device):
-            try:
+        err, h = "", b""
+        try:                             # any failure is reported to every rank below
+            with torch.cuda.device(self.device):
                 self._mb, h = xchg_alloc(self._flag_off + 128)
-            except Exception as e:       # noqa: BLE001 -- reported to every rank below
-                h, err = b"", f"alloc: {e}"
-            handles = [None] * P
-            dist.all_gather_object(handles, h, group=group)
-            if not err and r + 1 < P and handles[r + 1]:
+        except Exception as e:           # noqa: BLE001
+            err = f"alloc: {e}"
+        handles = [None] * P
+        dist.all_gather_object(handles, h, group=group)
+        if not err and r + 1 < P:
+            if not handles[r + 1]:
+                err = "next rank has no mailbox"
+            else:
                 try:
-                    self._peer = xchg_open(handles[r + 1])
+                    with torch.cuda.device(self.device):
+                        self._peer = xchg_open(handles[r + 1])
                 except Exception as e:   # noqa: BLE001
                     err = f"open: {e}"
         # every rank must agree, or the ranks would run different exchanges

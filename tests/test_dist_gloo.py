@@ -113,3 +113,43 @@ def test_lpt_assign_balances_and_partitions():
         loads = [int(sizes[part].sum()) for part in parts]
         assert max(loads) - min(loads) <= int(sizes.max())            # LPT bound: gap <= largest job
     assert lpt_assign([5, 5, 5], 2) == [[0, 2], [1]]
+
+
+def _p2p_agree_worker(rank, P, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        import paper_2505_21194_b200 as sc
+        from paper_2505_21194_b200.dist import CudaRangeBackend
+        be = CudaRangeBackend(sc.SeqParams.table1(8), device="cuda:0")
+        ok = be.enable_p2p()
+        res = [None] * P
+        dist.all_gather_object(res, (rank, ok, be.p2p, getattr(be, "p2p_error", "")))
+        if rank == 0:
+            q.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_p2p_mode_agreement_without_gpu(P):
+    """The fused exchange is switched on only if every rank mapped its peer's
+    mailbox: here (no GPU) every allocation fails, each rank's error reaches all
+    ranks and all of them stay on the collective exchange (no rank is left in
+    the fused protocol while another waits in an all_gather)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("needs a box without a GPU (with one, the mailboxes map; see test_gpu_range.py p2p cases)")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_agree_worker, args=(r, P, port, q)) for r in range(P)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert len(res) == P
+    for rank, ok, p2p, err in res:
+        assert ok is False and p2p is False and err, (rank, ok, p2p, err)
