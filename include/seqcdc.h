@@ -291,7 +291,22 @@ int seqcdc_range_merge_tail(const uint8_t *d_buf, uint64_t buf_len, uint64_t ran
  * UINT64_MAX, so d_sum3[0] != d_sum3[2] and the caller falls back to the
  * collective protocol.  flag_value must increase from call to call (a step
  * counter); the mailbox is reused. */
+/* seqcdc_xchg_put_rows / seqcdc_xchg_wait_rows: a small all-gather over peer
+ * memory (the step's second exchange).  Each rank's table holds nranks rows of
+ * nwords + 1 uint64; put_rows stores d_src[0..nwords) into row `row` of every
+ * rank's table (d_tables: a DEVICE array of nranks table addresses, mapped with
+ * seqcdc_xchg_open, this rank's own included) and then releases `step` into the
+ * row's last word; wait_rows waits on the device until every row of this
+ * rank's table carries `step`, copies the rows' data packed into d_out
+ * (optional, nranks * nwords uint64) and writes *d_status = 0 (1 after
+ * timeout_ns, d_out untouched).
+ * `step` must change from call to call; callers alternate two tables so that
+ * a rank one step ahead never overwrites a row still being read. */
 #define SEQCDC_IPC_HANDLE_BYTES 64
+int seqcdc_xchg_put_rows(const uint64_t *d_src, uint32_t nwords, uint64_t *const *d_tables, uint32_t nranks,
+                         uint32_t row, uint64_t step, void *stream);
+int seqcdc_xchg_wait_rows(const uint64_t *d_table, uint32_t nwords, uint32_t nranks, uint64_t step,
+                          uint64_t timeout_ns, uint64_t *d_status, uint64_t *d_out, void *stream);
 int seqcdc_xchg_alloc(size_t bytes, void **d_buf, void *ipc_handle);
 int seqcdc_xchg_open(const void *ipc_handle, void **d_peer);
 int seqcdc_xchg_close(void *d_peer);

@@ -34,7 +34,7 @@ EXPORTS = (
     "seqcdc_range_max_cuts", "seqcdc_range_chunk", "seqcdc_range_resync", "seqcdc_range_resync_dev",
     "seqcdc_range_chunk_tail", "seqcdc_range_merge_tail",
     "seqcdc_xchg_alloc", "seqcdc_xchg_open", "seqcdc_xchg_close", "seqcdc_xchg_free",
-    "seqcdc_range_chunk_tail_push", "seqcdc_range_merge_tail_wait",
+    "seqcdc_range_chunk_tail_push", "seqcdc_range_merge_tail_wait", "seqcdc_xchg_put_rows", "seqcdc_xchg_wait_rows",
     "seqcdc_fingerprint", "seqcdc_dedup_workspace_size", "seqcdc_dedup",
 )
 
@@ -136,6 +136,10 @@ def lib():
         L.seqcdc_range_chunk_tail_push.restype = ctypes.c_int
         L.seqcdc_range_merge_tail_wait.argtypes = [p, u64, u64, u64, P, p, u32, p, p, p, p, p, p, p, p, u64, u64, p]
         L.seqcdc_range_merge_tail_wait.restype = ctypes.c_int
+        L.seqcdc_xchg_put_rows.argtypes = [p, u32, p, u32, u32, u64, p]
+        L.seqcdc_xchg_put_rows.restype = ctypes.c_int
+        L.seqcdc_xchg_wait_rows.argtypes = [p, u32, u32, u64, u64, p, p, p]
+        L.seqcdc_xchg_wait_rows.restype = ctypes.c_int
         L.seqcdc_fingerprint.argtypes = [p, p, p, u64, p, p]
         L.seqcdc_fingerprint.restype = ctypes.c_int
         L.seqcdc_dedup_workspace_size.argtypes = [u64]
@@ -444,3 +448,23 @@ def range_merge_tail_wait_into(buf, range_len: int, global_offset: int, p: SeqPa
                                             sum3.data_ptr() if sum3 is not None else None, flag, int(flag_value),
                                             int(timeout_ns), _stream_ptr(stream, buf.device))
     _check(rc, "seqcdc_range_merge_tail_wait")
+
+
+def xchg_put_rows_into(src, tables, row: int, step: int, stream=None) -> None:
+    """Store ``src`` (int64 CUDA [nwords]) into row ``row`` of every rank's table
+    (``tables``: int64 CUDA [nranks] of mapped table addresses) and release
+    ``step`` behind it."""
+    _require_cuda(src, "src")
+    _check(lib().seqcdc_xchg_put_rows(src.data_ptr(), src.numel(), tables.data_ptr(), tables.numel(), row,
+                                      int(step), _stream_ptr(stream, src.device)), "seqcdc_xchg_put_rows")
+
+
+def xchg_wait_rows_into(table: int, nwords: int, nranks: int, step: int, status, out=None,
+                        timeout_ns: int = 10_000_000_000, stream=None) -> None:
+    """Wait on the device until all rows of this rank's table (device address)
+    carry ``step``; the rows' data packed into ``out`` (int64 CUDA
+    [nranks*nwords], optional); ``status`` (int64 CUDA [1]) = 0, or 1 on timeout."""
+    _require_cuda(status, "status")
+    _check(lib().seqcdc_xchg_wait_rows(table, nwords, nranks, int(step), int(timeout_ns), status.data_ptr(),
+                                       out.data_ptr() if out is not None else None,
+                                       _stream_ptr(stream, status.device)), "seqcdc_xchg_wait_rows")

@@ -1476,6 +1476,65 @@ SEQCDC_API int seqcdc_range_chunk_tail_push(const uint8_t *d_buf, uint64_t buf_l
 }
 
 // ------------------------------------------------------------------ peer-memory mailboxes (CUDA IPC)
+namespace seqcdc {
+// a small row stored into every rank's table (tables[p] = rank p's table, mapped
+// into this process); the row's last word is the step, released at system scope
+// after the data, so a reader that sees the step sees the row
+__global__ void k_put_rows(const uint64_t *src, uint32_t nwords, uint64_t *const *tables, uint32_t P, uint32_t r,
+                           uint64_t step)
+{
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    uint64_t *row = tables[p] + (uint64_t)r * (nwords + 1);
+    for (uint32_t i = 0; i < nwords; i++) row[i] = src[i];
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(row + nwords), "l"(step) : "memory");
+}
+
+// wait until every row of this rank's table carries `step` (acquire), at most
+// timeout_ns; *status = 0 when complete, 1 on timeout
+__global__ void k_wait_rows(const uint64_t *table, uint32_t nwords, uint32_t P, uint64_t step, uint64_t timeout_ns,
+                            uint64_t *status, uint64_t *out)
+{
+    uint64_t t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (uint32_t p = 0; p < P; p++) {
+        const uint64_t *f = table + (uint64_t)p * (nwords + 1) + nwords;
+#pragma unroll 1
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+            if (v == step) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > timeout_ns) {
+                *status = 1;
+                return;
+            }
+            __nanosleep(500);
+        }
+    }
+    if (out)                                  // the rows' data, packed, for the caller's one host read
+        for (uint32_t p = 0; p < P; p++)
+            for (uint32_t i = 0; i < nwords; i++) out[(uint64_t)p * nwords + i] = table[(uint64_t)p * (nwords + 1) + i];
+    *status = 0;
+}
+}  // namespace seqcdc
+
+SEQCDC_API int seqcdc_xchg_put_rows(const uint64_t *d_src, uint32_t nwords, uint64_t *const *d_tables,
+                                    uint32_t nranks, uint32_t row, uint64_t step, void *stream)
+{
+    if (!d_src || !d_tables || !nranks || row >= nranks || !nwords) return SEQCDC_EINVAL;
+    k_put_rows<<<(nranks + 31) / 32, 32, 0, (cudaStream_t)stream>>>(d_src, nwords, d_tables, nranks, row, step);
+    return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
+}
+
+SEQCDC_API int seqcdc_xchg_wait_rows(const uint64_t *d_table, uint32_t nwords, uint32_t nranks, uint64_t step,
+                                     uint64_t timeout_ns, uint64_t *d_status, uint64_t *d_out, void *stream)
+{
+    if (!d_table || !d_status || !nranks || !nwords) return SEQCDC_EINVAL;
+    k_wait_rows<<<1, 1, 0, (cudaStream_t)stream>>>(d_table, nwords, nranks, step, timeout_ns, d_status, d_out);
+    return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
+}
+
 SEQCDC_API int seqcdc_xchg_alloc(size_t bytes, void **d_buf, void *ipc_handle)
 {
     if (!d_buf || !ipc_handle || !bytes) return SEQCDC_EINVAL;

@@ -139,8 +139,11 @@ def _device_round(shard, backend, group, P, r):
         blocks = _allgather_dev(spec.extra["block"], group)     # [P, 3 + E]
         cur = backend.merge_dev(shard, blocks[r - 1], spec) if r > 0 else spec
     s3 = cur.extra["sum3"] if r > 0 else spec.extra["block"][[0, 1, 0]]   # rank 0's chain is final
-    info = _allgather_dev(s3, group)                        # [P, 3] = final ov, count, speculative ov
-    h = info.reshape(-1).cpu().tolist()
+    if getattr(backend, "p2p", False):                      # rows stored into every rank's table, one host read
+        h = backend.exchange_rows(s3, step)
+    else:
+        info = _allgather_dev(s3, group)                    # [P, 3] = final ov, count, speculative ov
+        h = info.reshape(-1).cpu().tolist()
     if any(h[3 * k] != h[3 * k + 2] for k in range(P)):     # an overhang changed: more rounds needed
         return None
     counts = [h[3 * k + 1] for k in range(P)]
@@ -185,36 +188,47 @@ class CudaRangeBackend:
         self._key = None
         self.p2p = False                 # fused exchange over peer memory (enable_p2p)
         self._mb = self._peer = None
+        self._peers = {}
         self._step = 0
 
     # ---- fused exchange over peer memory (SURVEY.md 8(e) "fused alternative")
-    def enable_p2p(self, group=None) -> None:
-        """Give this rank a device mailbox (CUDA IPC) and map the next rank's, so
-        the exchange block travels by peer stores from inside rank r's last kernel
-        to rank r+1 (NVLink between GPUs), with a device-side flag instead of the
-        first all_gather.  Collective: every rank calls it once."""
+    def enable_p2p(self, group=None) -> bool:
+        """Give this rank a device mailbox (CUDA IPC) and map every other rank's,
+        so that both exchanges of a step travel by peer stores (NVLink between
+        GPUs) with device-side flags: rank r's last kernel stores its tail block
+        into rank r+1's mailbox, and each rank stores its (overhang, count,
+        speculative overhang) row into every rank's table -- no collective and
+        no host involvement until the one host read of the table.  Collective:
+        every rank calls it once; it is on only if every rank mapped every peer."""
         from . import xchg_alloc, xchg_open
         P, r = dist.get_world_size(group), dist.get_rank(group)
         if P < 2:
             return False
+        self._P, self._r = P, r
         self._flag_off = ((8 * (3 + self.TAIL) + 127) // 128) * 128
+        self._tab_off = self._flag_off + 128                 # two tables (step parity) of P rows x 4 words
+        nbytes = self._tab_off + 2 * P * 32
         err, h = "", b""
         try:                             # any failure is reported to every rank below
             with torch.cuda.device(self.device):
-                self._mb, h = xchg_alloc(self._flag_off + 128)
+                self._mb, h = xchg_alloc(nbytes)
         except Exception as e:           # noqa: BLE001
             err = f"alloc: {e}"
         handles = [None] * P
         dist.all_gather_object(handles, h, group=group)
-        if not err and r + 1 < P:
-            if not handles[r + 1]:
-                err = "next rank has no mailbox"
-            else:
-                try:
-                    with torch.cuda.device(self.device):
-                        self._peer = xchg_open(handles[r + 1])
-                except Exception as e:   # noqa: BLE001
-                    err = f"open: {e}"
+        bases = [0] * P
+        if not err:
+            bases[r] = self._mb
+            try:
+                with torch.cuda.device(self.device):
+                    for q in range(P):
+                        if q != r:
+                            if not handles[q]:
+                                raise RuntimeError(f"rank {q} has no mailbox")
+                            self._peers[q] = xchg_open(handles[q])
+                            bases[q] = self._peers[q]
+            except Exception as e:       # noqa: BLE001
+                err = f"open: {e}"
         # every rank must agree, or the ranks would run different exchanges
         errs = [None] * P
         dist.all_gather_object(errs, err, group=group)
@@ -223,18 +237,46 @@ class CudaRangeBackend:
         if not self.p2p:
             self.close()
             self.p2p_error = next(e for e in errs if e)
-        return self.p2p
+            return False
+        self._peer = bases[r + 1] if r + 1 < P else None
+        # per step parity: the device array of every rank's table, and this rank's own
+        self._tables = [torch.tensor([b + self._tab_off + k * P * 32 for b in bases], dtype=torch.int64,
+                                     device=self.device) for k in range(2)]
+        self._tabdev = torch.zeros(P * 3 + 1, dtype=torch.int64, device=self.device)   # rows, then status
+        self._tabhost = torch.empty(P * 3 + 1, dtype=torch.int64, pin_memory=True)
+        return True
+
+    def exchange_rows(self, sum3, step: int, timeout_ns: int = 10_000_000_000) -> list[int]:
+        """The step's second exchange over peer memory: store this rank's row
+        (final overhang, count, speculative overhang) into every rank's table,
+        wait for all rows of this step on the device, then one host read.
+        Returns the P x 3 values row-major (raises after the timeout)."""
+        from . import xchg_put_rows_into, xchg_wait_rows_into
+        P, k = self._P, step & 1
+        with torch.cuda.device(self.device):
+            xchg_put_rows_into(sum3.contiguous(), self._tables[k], self._r, step, stream=self.stream)
+            own = self._mb + self._tab_off + k * P * 32
+            xchg_wait_rows_into(own, 3, P, step, self._tabdev[P * 3:], out=self._tabdev[: P * 3],
+                                timeout_ns=timeout_ns, stream=self.stream)
+            st = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+            with torch.cuda.stream(st):
+                self._tabhost.copy_(self._tabdev, non_blocking=True)
+            st.synchronize()
+        h = self._tabhost.tolist()
+        if h[P * 3] != 0:
+            raise RuntimeError("peer-memory exchange timed out (a rank stopped responding)")
+        return h[: P * 3]
 
     def next_step(self) -> int:
         self._step += 1
         return self._step
 
     def close(self) -> None:
-        """Unmap the peer mailbox and free this rank's (after all ranks are done)."""
+        """Unmap the peer mailboxes and free this rank's (after all ranks are done)."""
         from . import xchg_close, xchg_free
-        if self._peer is not None:
-            xchg_close(self._peer)
-            self._peer = None
+        for q in list(self._peers):
+            xchg_close(self._peers.pop(q))
+        self._peer = None
         if self._mb is not None:
             xchg_free(self._mb)
             self._mb = None

@@ -327,3 +327,31 @@ def test_fused_push_and_wait_single_process():
     finally:
         torch.cuda.synchronize()
         sc.xchg_free(mb)
+
+
+def test_peer_rows_exchange_single_process():
+    """seqcdc_xchg_put_rows / seqcdc_xchg_wait_rows (the step's second exchange
+    over peer memory), three 'ranks' whose tables live in one local mailbox:
+    every table receives every row, the wait returns the rows packed, and a
+    step that never arrives times out (status 1) instead of hanging."""
+    P, nw = 3, 3
+    mb, _ = sc.xchg_alloc(4096)
+    try:
+        tables = torch.tensor([mb + 1024 * q for q in range(P)], dtype=torch.int64, device="cuda")
+        rows = [torch.tensor([100 * r + 1, 100 * r + 2, 100 * r + 3], dtype=torch.int64, device="cuda")
+                for r in range(P)]
+        for r in range(P):
+            sc.xchg_put_rows_into(rows[r], tables, r, 5)
+        for q in range(P):
+            out = torch.full((P * nw,), -7, dtype=torch.int64, device="cuda")
+            status = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+            sc.xchg_wait_rows_into(mb + 1024 * q, nw, P, 5, status, out=out, timeout_ns=1_000_000_000)
+            assert int(status.item()) == 0
+            assert out.cpu().tolist() == [100 * r + i for r in range(P) for i in (1, 2, 3)]
+        status = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+        out = torch.full((P * nw,), -7, dtype=torch.int64, device="cuda")
+        sc.xchg_wait_rows_into(mb, nw, P, 6, status, out=out, timeout_ns=2_000_000)
+        assert int(status.item()) == 1 and out.cpu().tolist() == [-7] * (P * nw)
+    finally:
+        torch.cuda.synchronize()
+        sc.xchg_free(mb)
