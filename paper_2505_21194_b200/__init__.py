@@ -86,6 +86,10 @@ def lib():
         if not os.path.exists(path):
             raise SeqCDCError(f"libseqcdc.so missing at {path}; run __graft_entry__.build()")
         L = ctypes.CDLL(path)
+        missing = [name for name in EXPORTS if not hasattr(L, name)]
+        if missing:                      # e.g. a stale tuning build: fail now, not in a subprocess later
+            raise SeqCDCError(f"{path} lacks {', '.join(missing)}: rebuild it (__graft_entry__.build() or "
+                              f"tools/variants.sh)")
         u32, u64, p, sz = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t
         P = ctypes.POINTER(_CParams)
         L.seqcdc_validate_params.argtypes = [P]
