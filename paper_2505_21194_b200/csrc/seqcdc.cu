@@ -800,12 +800,25 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
     const uint32_t tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     int ok = 1;
-    for (uint32_t i = tid; i < k; i += blockDim.x) {
-        const int32_t t = __ldcg(w.target + i);
-        tg[i] = t;
-        cnt[i] = (uint64_t)__ldcg(w.midx + i);
-        en[i] = ENTRY_DEAD;
-        if (i + 1 < k && t != (int32_t)(i + 1)) ok = 0;
+    // one round of loads for everything per segment: the targets/merge indices go
+    // to shared memory, the list counts stay in registers for the count pass
+    // (launched with exactly 1024 threads; PER strides cover STITCH_MAX_SEGS)
+    constexpr int PER = (STITCH_MAX_SEGS + 1023) / 1024;
+    uint32_t lcv[PER], xcv[PER];
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+        const uint32_t i = tid + 1024u * u;
+        lcv[u] = xcv[u] = 0;
+        if (i < k) {
+            const int32_t t = __ldcg(w.target + i);
+            const int64_t m = __ldcg(w.midx + i);
+            lcv[u] = (uint32_t)(__ldcg(w.Lcnt + i) & CNT_MASK);
+            xcv[u] = __ldcg(w.Xcnt + i) + __ldcg(w.cont_cnt + i);
+            tg[i] = t;
+            cnt[i] = (uint64_t)m;
+            en[i] = ENTRY_DEAD;
+            if (i + 1 < k && t != (int32_t)(i + 1)) ok = 0;
+        }
     }
     ok = __syncthreads_and(ok);
     if (ok) {                                   // every extension merged into its successor
@@ -835,11 +848,13 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
         }
     }
     __syncthreads();
-    for (uint32_t i = tid; i < k; i += blockDim.x) {
-        const int64_t e = en[i];
-        cnt[i] = e == ENTRY_DEAD ? 0
-                                 : (__ldcg(w.Lcnt + i) & CNT_MASK) - (uint64_t)(e + 1) + __ldcg(w.Xcnt + i) +
-                                       __ldcg(w.cont_cnt + i);
+#pragma unroll
+    for (int u = 0; u < PER; u++) {
+        const uint32_t i = tid + 1024u * u;
+        if (i < k) {
+            const int64_t e = en[i];
+            cnt[i] = e == ENTRY_DEAD ? 0 : (uint64_t)lcv[u] - (uint64_t)(e + 1) + xcv[u];
+        }
     }
     __syncthreads();
     const uint64_t last = cnt[k - 1];
@@ -893,11 +908,23 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
         const uint64_t nl = lc - (uint64_t)(e + 1);
         const uint64_t *Ls = w.L + g.Loff + (e + 1);
         const uint64_t add = w.out_add;
-#pragma unroll 4
-        for (uint64_t i = lane; i < nl; i += 32) out[i] = __ldcg(Ls + i) + add;
+        // speculative list then extension list, 8 loads in flight per lane before
+        // their stores (one memory round trip per 256 cuts instead of per 32)
         const uint64_t *Xs = w.X + g.Xoff;
-#pragma unroll 2
-        for (uint64_t i = lane; i < nx; i += 32) out[nl + i] = __ldcg(Xs + i) + add;
+#pragma unroll 1
+        for (uint64_t i0 = 0; i0 < nl + nx; i0 += 256) {
+            uint64_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint64_t i = i0 + 32 * u + lane;
+                v[u] = i < nl ? __ldcg(Ls + i) : (i < nl + nx ? __ldcg(Xs + (i - nl)) : 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint64_t i = i0 + 32 * u + lane;
+                if (i < nl + nx) out[i] = v[u] + add;
+            }
+        }
         if (nc) {
             const uint64_t *Cs = cont_slot(w, s2, __ldcg(Xs + nx - 1));
             for (uint64_t i = lane; i < nc; i += 32) out[nl + nx + i] = __ldcg(Cs + i) + add;
