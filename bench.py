@@ -4,380 +4,55 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one seqcdc chunking call over the whole workload (every row of
-SURVEY.md 8(a): stage, classify, candidates/opposing counts, resolve, speculative
-segments, seam fixup, compact).  N=1 workload = BASELINE config 2 (configs[1]):
-a 1 GiB order-1 Markov text stream, Decreasing mode, SeqLength 5, SkipTrigger 55,
-SkipSize 256, min 2 KiB, max 8 KiB.  N>1 (torchrun, one rank per GPU): weak
-scaling, one N GiB stream of the same generator sharded into contiguous 1 GiB
-ranges, stitched with the range API + an NCCL all_gather (see
-paper_2505_21194_b200/dist.py).
+Workload = BASELINE config 5, the configuration the metric is quoted on: one
+64 GiB stream (50/50 uniform random bytes and +-1 ramps of length 2-600, seed
+5), Increasing, SeqLength 5, SkipTrigger 50, SkipSize 256, min 4 KiB, max
+16 KiB.  One step = one pass of the whole hot path over the whole stream
+(stage, classify, candidates, resolve, speculative segments, seam fix-up,
+compact).  N=1: the stream resident in one GPU's HBM, one
+seqcdc_chunk call per step.  N>1 (torchrun, one rank per GPU): the SAME stream
+sharded into N contiguous ranges (strong scaling), stitched by the seam
+protocol.  Every run checks the whole cut list against the CPU oracle.
 
+Implementation in benchlib/ (bench infrastructure, not product code).
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
-import json
 import os
-import platform
 import sys
-import threading
-import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-
-METRIC = "SeqCDC chunking GB/s at 1/2/4/8 B200; % of HBM-read roofline; cuts bit-exact"
-GiB = 1 << 30
-CFG2 = dict(kind="markov", seed=2, mode=1, avg_kib=4)
-WORKLOAD = ("config 2: order-1 Markov text stream (seeded 60-symbol model, ~5% repeated-token spans), "
-            "Decreasing mode, SeqLength=5, SkipTrigger=55, SkipSize=256, min 2 KiB, max 8 KiB")
-
-
-def _peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
-    except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
-
-
-# ------------------------------------------------------------------ clocks during the timed region
-class ClockSampler:
-    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
-               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks",
-               0x1: "gpu_idle", 0x10: "sync_boost"}
-
-    def __init__(self, index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self._nv = None
-
-    def _run(self):
-        nv = self._nv
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.002)
-
-    def __enter__(self):
-        if self._nv:
-            self._t = threading.Thread(target=self._run, daemon=True)
-            self._t.start()
-        return self
-
-    def __exit__(self, *a):
-        self._stop.set()
-        if self._nv:
-            self._t.join()
-
-    def summary(self):
-        s = sorted(self.samples)
-        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(s)}
-
-
-WORKLOAD_KEY = "config 2, 1 GiB Markov, Decreasing, Table I 4 KiB row"
-
-
-def _traffic(kernel, workload_key):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
-    (profiles/traffic.json), if it was taken on this workload."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            d = json.load(f)[kernel]
-        if d.get("workload") != workload_key:
-            return None, None
-        return int(d["dram_read_bytes"]) + int(d["dram_write_bytes"]), d.get("source")
-    except Exception:
-        return None, None
-
-
-def _cpu_desc():
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
-    except Exception:
-        pass
-    return platform.processor()
-
-
-# ------------------------------------------------------------------ oracle legs (host cores)
-def _host_workload(n: int):
-    """Config-2 bytes on the host, generated in parallel block ranges."""
-    import numpy as np
-    from concurrent.futures import ThreadPoolExecutor
-    import synth
-    out = np.empty(n, dtype=np.uint8)
-    piece = 32 << 20
-    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1)) as ex:
-        list(ex.map(lambda a: synth.fill_host(CFG2["kind"], CFG2["seed"], a, min(piece, n - a), out[a:a + piece]),
-                    range(0, n, piece)))
-    return out
-
-
-def _oracle_params():
-    import oracle
-    return oracle.table1(CFG2["avg_kib"], CFG2["mode"])
-
-
-def time_oracle(host_bytes, budget_s: float = 12.0, max_passes: int = 4):
-    """The oracle as it stands (single-threaded C), timed on this host over
-    whole passes of the workload until ~budget_s."""
-    import oracle
-    p = _oracle_params()
-    t_tot, passes, cuts = 0.0, 0, None
-    while passes < max_passes and (passes == 0 or t_tot < budget_s):
-        t0 = time.perf_counter()
-        cuts = oracle.chunk(host_bytes, p)
-        t_tot += time.perf_counter() - t0
-        passes += 1
-    return host_bytes.size * passes / t_tot / 1e9, passes, t_tot, cuts
-
-
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    n = args.bytes_per_gpu
-    host = _host_workload(n)
-    import oracle
-    p = _oracle_params()
-    # each step = one oracle pass over a bounded sample (whole stream if it fits the budget)
-    t0 = time.perf_counter()
-    oracle.chunk(host[: min(n, 64 << 20)], p)
-    est = (time.perf_counter() - t0) * n / min(n, 64 << 20)
-    budget = 150.0
-    sample = n if est * (args.steps + args.warmup) <= budget else \
-        max(16 << 20, int(n * budget / (est * (args.steps + args.warmup))) & ~0xFFFFF)
-    view = host[:sample]
-    for _ in range(args.warmup):
-        oracle.chunk(view, p)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        cuts = oracle.chunk(view, p)
-    dt = time.perf_counter() - t0
-    value = sample * args.steps / dt / 1e9
-    sample_desc = (f"first {sample} bytes of the {n}-byte config-2 stream per step" if sample < n
-                   else f"whole {n}-byte config-2 stream per step")
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "stream_bytes": n, "sample_bytes": sample},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": sample_desc, "cpu": _cpu_desc(), "host_cores": os.cpu_count(),
-                         "ncuts": int(cuts.size)},
-        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "the CPU oracle (plain single-threaded C, gcc -O2) is the reference arm: no reference code exists",
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-# ------------------------------------------------------------------ our arm, one GPU
-def run_single(args):
-    import numpy as np
-    import torch
-    import synth
-    import paper_2505_21194_b200 as sc
-
-    dev = torch.device("cuda", 0)
-    torch.cuda.set_device(dev)
-    n = args.bytes_per_gpu
-    p = sc.SeqParams.table1(CFG2["avg_kib"], CFG2["mode"])
-    data = torch.empty(n, dtype=torch.uint8, device=dev)
-    synth.fill_device(CFG2["kind"], CFG2["seed"], 0, data)
-    cuts = torch.empty(sc.max_cuts(n, p), dtype=torch.int64, device=dev)
-    ncuts = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = torch.empty(sc.workspace_size(n, 1, p), dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    torch.cuda.synchronize()
-
-    def step():
-        sc.chunk_into(data, p, cuts, ncuts, workspace=ws, stream=stream)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    value = n / (ms / 1e3) / 1e9
-    k = int(ncuts.item())
-    # kernel share: a second timed region of the same K steps with per-phase CUDA
-    # events recorded by the library on the launching stream (they also disable the
-    # programmatic launch overlap of the post kernel, so this region is slightly slower)
-    sc.profile_enable(True)
-    for _ in range(args.steps):
-        step()
-    torch.cuda.synchronize()
-    prof, ncalls = sc.profile_collect()
-    sc.profile_enable(False)
-    walk_ms = prof["walk"] / max(ncalls, 1)
-    peak, peak_src = _peaks()
-    achieved = n / (walk_ms / 1e3) / 1e9
-    traffic, traffic_src = _traffic("k_walk", WORKLOAD_KEY)
-
-    # ---- end to end through the public API with host buffers (pinned), H2D + D2H inside the region
-    host_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    host_in.copy_(data.cpu())
-    host_cuts = torch.empty(cuts.numel(), dtype=torch.int64, pin_memory=True)
-    host_n = torch.empty(1, dtype=torch.int64, pin_memory=True)
-    e2e_steps = max(2, min(args.steps, 8))
-    d2h_bytes = 0
-    for it in range(1 + e2e_steps):
-        if it == 1:
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-        data.copy_(host_in, non_blocking=True)
-        step()
-        host_n.copy_(ncuts, non_blocking=True)
-        torch.cuda.synchronize()           # result count needed to size the cut read-back
-        kk = int(host_n.item())
-        host_cuts[:kk].copy_(cuts[:kk], non_blocking=True)
-        torch.cuda.synchronize()
-        d2h_bytes = 8 + 8 * kk
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_value = n / e2e_s / 1e9
-
-    # ---- parity of the timed output against the oracle (whole list) + CPU baseline
-    host_bytes = host_in.numpy()
-    cpu_value, passes, cpu_t, want = time_oracle(host_bytes, budget_s=10.0, max_passes=64)
-    got = cuts[:k].cpu().numpy().astype(np.uint64)
-    exact = bool(got.size == want.size and np.array_equal(got, want))
-    del host_in, host_cuts
-    read_peak = measure_read_peak(data, stream)
-    ns4 = north_star_4gib(args, dev, stream, read_peak) if not args.skip_4gib else None
-
-    line = {
-        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "stream_bytes": n, "parallelism": "single GPU, segment-speculative",
-                   "l2": "input 1 GiB > 126 MB L2: no flush needed between steps",
-                   "ncuts": k, "mean_chunk": round(n / max(k, 1), 1), "lib": sc.build_info()},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
-                     "kernel": "k_walk", "kernel_ms": round(walk_ms, 4), "algorithmic_bytes": n,
-                     "peak_source": peak_src, "share_of_step": round(walk_ms / prof["call"] * ncalls, 3),
-                     "kernel_timing": "CUDA events around k_walk on the launching stream, second region of K steps"},
-        "phases_ms": {k2: round(v / max(ncalls, 1), 4) for k2, v in prof.items()},
-        "cpu_baseline": {"value": round(cpu_value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"whole config-2 stream x{passes} passes ({cpu_t:.1f} s)",
-                         "cpu": _cpu_desc(), "host_cores": os.cpu_count()},
-        "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": n,
-                "d2h_bytes_per_step": d2h_bytes,
-                "how": "pinned host -> device copy, seqcdc_chunk, device -> host cuts, per step"},
-        "clocks": clk.summary(),
-        "gpu_launches": 2 * args.steps,
-        "parity": {"vs_oracle": "whole cut list", "bit_exact": exact, "ncuts": k},
-        "read_only_peak": read_peak,
-        "north_star_4gib": ns4,
-    }
-    print(json.dumps(line), flush=True)
-    return 0 if exact and (ns4 is None or ns4["bit_exact"]) else 3
-
-
-def measure_read_peak(data, stream):
-    """A read-only HBM reference measured in this job: a torch
-    int64 sum over the resident 1 GiB input (reads every byte once); the
-    denominator `peak` above stays MEASURED_PEAKS.json's copy figure."""
-    import torch
-    v = data.view(torch.int64)
-    for _ in range(3):
-        v.sum()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(10):
-        v.sum()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / 10
-    return {"value": round(data.numel() / ms / 1e6, 1), "unit": "GB/s", "how": "torch.sum over the 1 GiB input as int64"}
-
-
-def north_star_4gib(args, dev, stream, read_peak):
-    """BASELINE north_star target: >= 60% of HBM read bandwidth for single-GPU
-    chunking of a >= 4 GiB stream.  Config-5 data shape (uniform / +-1 ramps),
-    Table I 8 KiB row, 4 GiB + 12345 bytes, inputs resident; every cut checked."""
-    import numpy as np
-    import torch
-    import synth
-    import oracle
-    import paper_2505_21194_b200 as sc
-    n = (4 << 30) + 12345
-    p = sc.SeqParams.table1(8, 0)
-    d = torch.empty(n, dtype=torch.uint8, device=dev)
-    synth.fill_device("rampmix", 5, 0, d)
-    cuts = torch.empty(sc.max_cuts(n, p), dtype=torch.int64, device=dev)
-    nc = torch.zeros(1, dtype=torch.int64, device=dev)
-    ws = torch.empty(sc.workspace_size(n, 1, p), dtype=torch.uint8, device=dev)
-    for _ in range(3):
-        sc.chunk_into(d, p, cuts, nc, workspace=ws, stream=stream)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(3, min(args.steps, 10))
-    e0.record(stream)
-    for _ in range(steps):
-        sc.chunk_into(d, p, cuts, nc, workspace=ws, stream=stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
-    got = cuts[: int(nc.item())].cpu().numpy().astype(np.uint64)
-    want = oracle.chunk(d.cpu().numpy(), oracle.table1(8, 0))
-    gbs = n / ms / 1e6
-    peak, src = _peaks()
-    del d, cuts, ws
-    torch.cuda.empty_cache()
-    return {"workload": "4 GiB + 12345 B rampmix (config-5 shape), Increasing, L5 T50 S256, min 4 KiB, max 16 KiB",
-            "value": round(gbs, 1), "unit": "GB/s", "ms_per_step": round(ms, 4), "steps": steps,
-            "frac_of_measured_copy_peak": round(gbs / peak, 4),
-            "frac_of_read_only_peak": round(gbs / read_peak["value"], 4),
-            "bit_exact": bool(np.array_equal(got, want)), "ncuts": int(got.size)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--bytes-per-gpu", type=int, default=GiB)
-    ap.add_argument("--skip-4gib", action="store_true", help="skip the north-star 4 GiB line")
+    ap.add_argument("--workload", default="cfg5", help="cfg5 (default, the metric's config) | cfg2 | rampmix4g")
+    ap.add_argument("--bytes", type=int, default=0, help="resize the workload (testing only)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary config-2 / 4 GiB lines")
+    ap.add_argument("--profile-only", action="store_true", help="timed calls only (for ncu runs)")
+    ap.add_argument("--cpu-budget", type=float, default=10.0, help="seconds of single-thread oracle timing")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
+    from benchlib.common import WORKLOADS
+    w = WORKLOADS[args.workload]
+    if args.bytes:
+        w = w.resized(args.bytes)
     if args.impl == "reference":
-        return run_reference(args)
+        from benchlib import reference
+        return reference.run(args, w)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus > 1 or world > 1:
-        from paper_2505_21194_b200 import dist_bench
-        return dist_bench.run(args, METRIC, WORKLOAD, CFG2)
-    return run_single(args)
+        from benchlib import multi
+        return multi.run(args, w)
+    from benchlib import single
+    return single.run(args, w)
 
 
 if __name__ == "__main__":

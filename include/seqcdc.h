@@ -337,6 +337,11 @@ int seqcdc_set_segment_bytes(uint64_t g);
 int seqcdc_profile_enable(int on);
 int seqcdc_profile_collect(double *ms, uint64_t *ncalls);
 
+/* Number of CUDA kernels this library has launched so far in this process
+ * (all entry points, all devices; monotone).  Host-only, never blocks.  The
+ * bench reports the difference across its timed region as its launch count. */
+uint64_t seqcdc_launch_count(void);
+
 /* Human-readable name of a return code (static string). */
 const char *seqcdc_strerror(int code);
 

@@ -102,6 +102,10 @@ def _load():
         lib.oracle_next_cut.argtypes = [p, u64, u64, u32, u32, u32, u32, u64, u64, u32, p]
         lib.oracle_chunk_batch.restype = ctypes.c_int64
         lib.oracle_chunk_batch.argtypes = [p, p, u32, u32, u32, u32, u32, u64, u64, u32, p, u64, p]
+        lib.oracle_chunk_window.restype = ctypes.c_int64
+        lib.oracle_chunk_window.argtypes = [p, u64, u64, u32, u32, u32, u32, u64, u64, u32, p, u64, p, p]
+        lib.oracle_check_params.restype = ctypes.c_int
+        lib.oracle_check_params.argtypes = [u32, u32, u32, u64, u64]
         _lib = lib
     return _lib
 
@@ -132,6 +136,47 @@ def chunk(data, p: Params, return_examined: bool = False):
         raise RuntimeError(f"oracle_chunk failed ({k})")
     out = cuts[:k].copy()
     return (out, int(ex.value)) if return_examined else out
+
+
+def check_params_c(p: Params) -> int:
+    """The C oracle's own parameter check (0 = accepted, 1 = rejected)."""
+    return int(_load().oracle_check_params(p.mode, p.seq_length, p.skip_trigger, p.min_size, p.max_size))
+
+
+class _Touch(ctypes.Structure):
+    _fields_ = [("nunits", ctypes.c_uint32), ("shift", ctypes.c_uint32 * 4), ("origin", ctypes.c_uint64),
+                ("first", ctypes.c_uint64 * 4), ("last", ctypes.c_uint64 * 4), ("count", ctypes.c_uint64 * 4)]
+
+
+NONE_U64 = (1 << 64) - 1
+
+
+def chunk_window(data, last_start: int, p: Params, origin: int = 0, unit_shifts=(5, 7, 9, 11)):
+    """Chunk ``data`` from offset 0 (a chunk start), stopping after the chunk
+    that starts beyond ``last_start`` (C ``oracle_chunk_window``).  Measurement
+    side: the compared pairs and, per unit size 2**shift, the distinct
+    ``origin``-aligned units their bytes lie in (the bytes the method reads,
+    SURVEY.md 8(d)).  Returns (cuts, pairs, {shift: (count, first, last)})."""
+    p.check()
+    b = _as_u8(data)
+    n = int(b.size)
+    cap = max_cuts(min(n, last_start + p.max_size), p) + 2
+    cuts = np.empty(cap, dtype=np.uint64)
+    ex = ctypes.c_uint64(0)
+    t = _Touch()
+    t.nunits = len(unit_shifts)
+    for g, sh in enumerate(unit_shifts):
+        t.shift[g] = sh
+        t.first[g] = t.last[g] = NONE_U64
+        t.count[g] = 0
+    t.origin = origin
+    k = _load().oracle_chunk_window(b.ctypes.data, n, last_start, p.mode, p.seq_length, p.skip_trigger,
+                                    p.skip_size, p.min_size, p.max_size, p.flags, cuts.ctypes.data, cap,
+                                    ctypes.addressof(ex), ctypes.addressof(t))
+    if k < 0:
+        raise RuntimeError(f"oracle_chunk_window failed ({k})")
+    touch = {sh: (int(t.count[g]), int(t.first[g]), int(t.last[g])) for g, sh in enumerate(unit_shifts)}
+    return cuts[:k].copy(), int(ex.value), touch
 
 
 def next_cut(data, base: int, p: Params) -> int:
@@ -267,6 +312,65 @@ def chunk_query(data, p: Params) -> np.ndarray:
         cuts.append(cut)
         base = cut
     return np.asarray(cuts, dtype=np.uint64)
+
+
+def touched_units_query(data, p: Params, unit_shifts=(5, 7, 9, 11)) -> dict:
+    """Measurement cross-check written in the query form: per chunk, the pairs
+    examined are the intervals [a, e] from each anchor a (then d+1+S after
+    each skip) to the pair that decides it (the run's last pair, the T-th
+    opposing pair, or limit-2); the units touched are those holding a byte of
+    [a, e+1].  Returns {shift: distinct unit count}.  Small inputs only."""
+    p.check()
+    b = _as_u8(data).view(np.int8).astype(np.int16) if p.signed else _as_u8(data).astype(np.int16)
+    n = int(b.size)
+    L, T, S = p.seq_length, p.skip_trigger, p.skip_size
+    diff = b[1:] - b[:-1] if n > 1 else np.zeros(0, dtype=np.int16)
+    fav, opn = (diff > 0, diff < 0) if p.mode == INCREASING else (diff < 0, diff > 0)
+    m = p.run_bytes - 1
+    intervals = []
+    base = 0
+    while base < n:
+        limit = min(base + p.max_size, n)
+        a = base + p.min_size - L
+        while True:
+            last_pair = limit - 2
+            if a > last_pair:
+                cut = limit
+                break
+            # first pair e >= a ending a run of m favourable pairs that starts at >= a
+            e_run = None
+            run = 0
+            e_opp = None
+            cnt = 0
+            for i in range(a, last_pair + 1):
+                run = run + 1 if fav[i] else 0
+                if run >= m:
+                    e_run = i
+                    break
+                if opn[i]:
+                    cnt += 1
+                    if cnt == T:
+                        e_opp = i
+                        break
+            if e_run is not None:
+                intervals.append((a, e_run + 1))
+                cut = e_run + 2
+                break
+            if e_opp is not None:
+                intervals.append((a, e_opp + 1))
+                a = e_opp + 1 + S
+                continue
+            intervals.append((a, last_pair + 1))
+            cut = limit
+            break
+        base = cut
+    out = {}
+    for sh in unit_shifts:
+        units = set()
+        for lo, hi in intervals:
+            units.update(range(lo >> sh, (hi >> sh) + 1))
+        out[sh] = len(units)
+    return out
 
 
 # --------------------------------------------------------------------------

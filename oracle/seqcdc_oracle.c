@@ -65,14 +65,44 @@ int oracle_check_params(uint32_t mode, uint32_t seq_length, uint32_t skip_trigge
 }
 
 /*
+ * Measurement only (SURVEY.md 8(d) "algorithmic bytes"): the distinct aligned
+ * units of 2^shift bytes (absolute stream offsets: origin + position) that hold
+ * a byte of some compared pair (i, i+1) -- the bytes the method itself reads.
+ * Pairs are visited in increasing i, so "distinct" is a running maximum.
+ * Does not influence any cut.
+ */
+#define ORACLE_TOUCH_MAX 4
+typedef struct {
+    uint32_t nunits;
+    uint32_t shift[ORACLE_TOUCH_MAX];
+    uint64_t origin;                       /* absolute offset of b[0] */
+    uint64_t first[ORACLE_TOUCH_MAX];      /* first unit touched (UINT64_MAX: none yet) */
+    uint64_t last[ORACLE_TOUCH_MAX];       /* last unit touched  (UINT64_MAX: none yet) */
+    uint64_t count[ORACLE_TOUCH_MAX];      /* distinct units touched */
+} oracle_touch_t;
+
+static void touch_byte(oracle_touch_t *t, uint64_t pos)
+{
+    for (uint32_t g = 0; g < t->nunits; g++) {
+        uint64_t u = (t->origin + pos) >> t->shift[g];
+        if (t->last[g] == UINT64_MAX || u > t->last[g]) {
+            if (t->first[g] == UINT64_MAX) t->first[g] = u;
+            t->last[g] = u;
+            t->count[g]++;
+        }
+    }
+}
+
+/*
  * One chunk: the cut that ends the chunk starting at `base` of the stream
  * b[0..n).  Requires base < n.  *examined (if non-null) is incremented by the
- * number of byte pairs compared (the oracle's "algorithmic work" counter).
+ * number of byte pairs compared (the oracle's "algorithmic work" counter);
+ * `touch` (if non-null) records the units those pairs' bytes lie in.
  */
-uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
-                         uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
-                         uint32_t skip_size, uint64_t min_size, uint64_t max_size,
-                         uint32_t flags, uint64_t *examined)
+static uint64_t next_cut_impl(const uint8_t *b, uint64_t n, uint64_t base,
+                              uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
+                              uint32_t skip_size, uint64_t min_size, uint64_t max_size,
+                              uint32_t flags, uint64_t *examined, oracle_touch_t *touch)
 {
     const uint32_t sgn = flags & 1u;               /* signed bytes (c6 alternative) */
     const uint32_t run_end = (flags & 2u) ? seq_length + 1 : seq_length;   /* bytes in a qualifying run (c1) */
@@ -86,6 +116,7 @@ uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
         int x = sgn ? (int)(int8_t)b[i] : (int)b[i];          /* unsigned bytes (c6) */
         int y = sgn ? (int)(int8_t)b[i + 1] : (int)b[i + 1];  /* or signed (flag)    */
         if (examined) (*examined)++;
+        if (touch) { touch_byte(touch, i); touch_byte(touch, i + 1); }
         int favourable, opposing;
         if (mode == 0) { favourable = x < y; opposing = x > y; }   /* Increasing */
         else           { favourable = x > y; opposing = x < y; }   /* Decreasing */
@@ -108,6 +139,15 @@ uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
             i += 1;
         }
     }
+}
+
+uint64_t oracle_next_cut(const uint8_t *b, uint64_t n, uint64_t base,
+                         uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
+                         uint32_t skip_size, uint64_t min_size, uint64_t max_size,
+                         uint32_t flags, uint64_t *examined)
+{
+    return next_cut_impl(b, n, base, mode, seq_length, skip_trigger, skip_size,
+                         min_size, max_size, flags, examined, 0);
 }
 
 /*
@@ -156,4 +196,32 @@ int64_t oracle_chunk_batch(const uint8_t *b, const uint64_t *offsets, uint32_t n
     }
     cut_index[ns] = total;
     return (int64_t)total;
+}
+
+/*
+ * Window form for checking a long cut list in independent pieces (measurement
+ * and parity infrastructure; same loop as oracle_chunk): chunk b[0..n) from
+ * offset 0 as a chunk start, stopping after the chunk that starts beyond
+ * `last_start` (a chunk starting at base is fixed by b[base .. base+max), P:179,
+ * P:189, so the caller passes n >= last_start + max_size unless b ends at
+ * the stream end).  `touch` (optional) accumulates the units the compared pairs
+ * touch.  Returns the number of cuts or -(error).
+ */
+int64_t oracle_chunk_window(const uint8_t *b, uint64_t n, uint64_t last_start,
+                            uint32_t mode, uint32_t seq_length, uint32_t skip_trigger,
+                            uint32_t skip_size, uint64_t min_size, uint64_t max_size,
+                            uint32_t flags, uint64_t *cuts, uint64_t cap,
+                            uint64_t *examined, oracle_touch_t *touch)
+{
+    if (oracle_check_params(mode, seq_length, skip_trigger, min_size, max_size))
+        return -ORACLE_EINVAL;
+    uint64_t k = 0, base = 0;
+    while (base < n && base <= last_start) {
+        uint64_t c = next_cut_impl(b, n, base, mode, seq_length, skip_trigger,
+                                   skip_size, min_size, max_size, flags, examined, touch);
+        if (k >= cap) return -ORACLE_ECAP;
+        cuts[k++] = c;
+        base = c;
+    }
+    return (int64_t)k;
 }

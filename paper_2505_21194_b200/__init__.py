@@ -35,7 +35,7 @@ EXPORTS = (
     "seqcdc_range_chunk_tail", "seqcdc_range_merge_tail",
     "seqcdc_xchg_alloc", "seqcdc_xchg_open", "seqcdc_xchg_close", "seqcdc_xchg_free",
     "seqcdc_range_chunk_tail_push", "seqcdc_range_merge_tail_wait", "seqcdc_xchg_put_rows", "seqcdc_xchg_wait_rows",
-    "seqcdc_fingerprint", "seqcdc_dedup_workspace_size", "seqcdc_dedup",
+    "seqcdc_fingerprint", "seqcdc_dedup_workspace_size", "seqcdc_dedup", "seqcdc_launch_count",
 )
 
 
@@ -112,6 +112,8 @@ def lib():
         L.seqcdc_build_info.restype = ctypes.c_char_p
         L.seqcdc_set_segment_bytes.argtypes = [u64]
         L.seqcdc_set_segment_bytes.restype = ctypes.c_int
+        L.seqcdc_launch_count.argtypes = []
+        L.seqcdc_launch_count.restype = u64
         L.seqcdc_profile_enable.argtypes = [ctypes.c_int]
         L.seqcdc_profile_enable.restype = ctypes.c_int
         L.seqcdc_profile_collect.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(u64)]
@@ -194,6 +196,11 @@ def profile_collect():
     n = ctypes.c_uint64(0)
     _check(lib().seqcdc_profile_collect(ms, ctypes.byref(n)), "seqcdc_profile_collect")
     return {"setup": ms[0], "walk": ms[1], "post": ms[2], "call": ms[3]}, int(n.value)
+
+
+def launch_count() -> int:
+    """Kernels the library has launched in this process so far (monotone)."""
+    return int(lib().seqcdc_launch_count())
 
 
 def build_info() -> str:

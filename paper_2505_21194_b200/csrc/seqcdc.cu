@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -966,6 +967,7 @@ struct Plan {
 };
 
 static int g_sms = 0;
+static std::atomic<uint64_t> g_launches{0};   // kernels this library has launched (process-wide)
 static uint64_t g_force_G = 0;
 static std::mutex g_mu;
 static cudaMemPool_t g_pool[64];
@@ -1163,6 +1165,7 @@ static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, 
     prof_mark(pr, 1, st);
     if (w.single) k_walk<MODE, MSPEC, true><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
     else k_walk<MODE, MSPEC, false><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
+    g_launches++;
     prof_mark(pr, 2, st);
     if (w.single) {
         // programmatic dependent launch: k_post's CTAs become resident on SMs the
@@ -1180,12 +1183,14 @@ static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, 
         cfg.attrs = at;
         cfg.numAttrs = 1;
         cudaLaunchKernelEx(&cfg, k_post, w);
+        g_launches++;
         return;
     }
     const uint32_t sgrid = (uint32_t)std::min<uint64_t>(w.ns, 2ull * sms);
     k_stitch<MODE, MSPEC><<<sgrid, 1024, STITCH_SMEM, st>>>(w);
     k_scan<<<1, 1024, 0, st>>>(w);
     k_copy<<<std::max(1, sms * 4), 256, 0, st>>>(w);
+    g_launches += 3;
 }
 
 struct TailReq {
@@ -1280,6 +1285,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
             return SEQCDC_ECUDA;
     } else {
         k_setup<<<1, 1024, 0, st>>>(w);
+        g_launches++;
     }
     const int ms = w.p.M == 4 ? 4 : (w.p.M < 4 ? 0 : -1);
     // MODE: bit 0 = Decreasing, bit 1 = signed-byte reading (flag)
@@ -1338,6 +1344,9 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
 }  // namespace seqcdc
 
 using namespace seqcdc;
+
+// kernel launches made by the other translation units
+void seqcdc_note_launches(int k) { g_launches += (uint64_t)k; }
 
 // the library's stream-ordered pool (no trimming at synchronisation), for the
 // other translation units' small per-call allocations
@@ -1426,6 +1435,7 @@ SEQCDC_API int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets
     cudaStream_t st = (cudaStream_t)stream;
     if (ns == 0) {
         k_empty<<<1, 1, 0, st>>>(d_cut_index, d_ncuts);
+        g_launches++;
         return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
     }
     return enqueue(d_in, d_offsets, ns, total, total, 0, p, d_cuts, d_cut_index, d_ncuts, d_ws, ws_bytes, st,
@@ -1465,6 +1475,7 @@ static int range_chunk_tail_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_
         if (tail_max && cudaMemsetAsync(d_tail_n, 0, 8, st) != cudaSuccess) return SEQCDC_ECUDA;
         if (d_summary) k_set2<<<1, 1, 0, st>>>(d_summary, global_offset + entry, 0);
         if (push_blk) k_push_empty<<<1, 1, 0, st>>>(push_blk, push_flag, global_offset + entry, push_value);
+        g_launches += (d_summary ? 1 : 0) + (push_blk ? 1 : 0);
         return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
     }
     if (!d_buf || !d_cuts) return SEQCDC_EINVAL;
@@ -1551,6 +1562,7 @@ SEQCDC_API int seqcdc_xchg_put_rows(const uint64_t *d_src, uint32_t nwords, uint
 {
     if (!d_src || !d_tables || !nranks || row >= nranks || !nwords) return SEQCDC_EINVAL;
     k_put_rows<<<(nranks + 31) / 32, 32, 0, (cudaStream_t)stream>>>(d_src, nwords, d_tables, nranks, row, step);
+    g_launches++;
     return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
 }
 
@@ -1559,6 +1571,7 @@ SEQCDC_API int seqcdc_xchg_wait_rows(const uint64_t *d_table, uint32_t nwords, u
 {
     if (!d_table || !d_status || !nranks || !nwords) return SEQCDC_EINVAL;
     k_wait_rows<<<1, 1, 0, (cudaStream_t)stream>>>(d_table, nwords, nranks, step, timeout_ns, d_status, d_out);
+    g_launches++;
     return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
 }
 
@@ -1649,6 +1662,11 @@ SEQCDC_API int seqcdc_profile_collect(double *ms, uint64_t *ncalls)
     if (ncalls) *ncalls = g_prof_recs.size();
     g_prof_recs.clear();
     return SEQCDC_OK;
+}
+
+SEQCDC_API uint64_t seqcdc_launch_count(void)
+{
+    return g_launches.load();
 }
 
 SEQCDC_API int seqcdc_set_segment_bytes(uint64_t g)

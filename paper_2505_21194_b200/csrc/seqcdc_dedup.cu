@@ -23,6 +23,7 @@
 #define SEQCDC_API extern "C" __attribute__((visibility("default")))
 // internal (seqcdc.cu): the library's memory pool (keeps its memory across syncs)
 int seqcdc_internal_pool(cudaMemPool_t *pool);
+void seqcdc_note_launches(int k);
 
 namespace seqcdc {
 namespace {
@@ -289,6 +290,7 @@ SEQCDC_API int seqcdc_fingerprint(const uint8_t *d_in, const uint64_t *d_cuts, c
     if (cudaMallocFromPoolAsync((void **)&next, 8, pool, st) != cudaSuccess) return SEQCDC_ENOMEM;
     cudaMemsetAsync(next, 0, 8, st);
     k_sha256<<<(unsigned)grid, 128, 0, st>>>(d_in, d_cuts, d_ncuts, max_cuts, d_digests, 1u, next);
+    seqcdc_note_launches(1);
     cudaFreeAsync(next, st);
     return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
 }
@@ -314,10 +316,12 @@ SEQCDC_API int seqcdc_dedup(const uint8_t *d_digests, const uint64_t *d_cuts, co
         owned = true;
     }
     k_dedup_clear<<<592, 256, 0, st>>>(table, cap, d_unique_bytes);
+    seqcdc_note_launches(1);
     if (max_cuts) {
         k_dedup_insert<<<592, 256, 0, st>>>(d_digests, d_ncuts, max_cuts, table, cap - 1);
         k_dedup_mark<<<592, 256, 0, st>>>(d_digests, d_cuts, d_ncuts, max_cuts, table, cap - 1, d_first,
                                           d_unique_bytes);
+        seqcdc_note_launches(2);
     }
     if (owned) cudaFreeAsync(table, st);
     return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;

@@ -24,6 +24,7 @@
 
 // internal (seqcdc.cu): the ring geometry every walker of a call uses
 void seqcdc_ring_geometry(const seqcdc_params_t *p, uint32_t *bs, uint32_t *nb, uint32_t *ah);
+void seqcdc_note_launches(int k);
 
 namespace seqcdc {
 namespace {
@@ -264,6 +265,7 @@ void launch(const ResyncArgs &a, cudaStream_t st)
 {
     k_resync<MODE, MSPEC><<<1, 32, 0, st>>>(a);
     k_resync_tail<<<148, 256, 0, st>>>(a);
+    seqcdc_note_launches(2);
 }
 
 template <int MODE>
@@ -353,6 +355,7 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
     cudaStream_t st = (cudaStream_t)stream;
     if (!d_entry && entry >= range_len) {
         k_resync_empty<<<1, 1, 0, st>>>(d_ncuts, d_status, global_offset + entry);
+        seqcdc_note_launches(1);
         return cudaGetLastError() == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
     }
     if (!d_buf || !d_cuts || !d_spec) return SEQCDC_EINVAL;
@@ -381,6 +384,7 @@ static int resync_impl(const uint8_t *d_buf, uint64_t buf_len, uint64_t range_le
     seqcdc_ring_geometry(p, &a.p.bs, &a.p.nb, &a.p.ah);
     if (merge_blk) {              // local merge first; the re-walk runs only if it found none
         k_merge_tail<<<1, 128, 0, st>>>(merge_blk, tail_max, a, g_wait_flag, g_wait_value, g_wait_timeout);
+        seqcdc_note_launches(1);
         a.skip = d_status;
     }
     const int ms = a.p.M == 4 ? 4 : (a.p.M < 4 ? 0 : -1);

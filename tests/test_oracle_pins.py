@@ -414,3 +414,82 @@ def test_pairs_reading_is_bytes_reading_shifted():
         if n <= 600:
             assert oracle.chunk_py(b, pp) == want.tolist()
             assert np.array_equal(oracle.chunk_query(b, pp), want)
+
+
+# ---------------------------------------------------------------- parameter validation
+@pytest.mark.parametrize("bad", [
+    dict(mode=2), dict(seq_length=1), dict(seq_length=0), dict(skip_trigger=0),
+    dict(seq_length=5, min_size=4), dict(min_size=100, max_size=99),
+])
+def test_check_params_rejects(bad):
+    """The oracle refuses what the method cannot mean: a mode other than
+    Increasing/Decreasing, a run shorter than 2 bytes, a skip
+    trigger of 0, min < SeqLength (the sub-minimum region min-L would be
+    negative) and max < min.  Both the C check and Params.check."""
+    base = dict(mode=0, seq_length=5, skip_trigger=50, skip_size=256, min_size=4096, max_size=16384)
+    base.update(bad)
+    p = oracle.Params(**base)
+    assert oracle.check_params_c(p) == 1
+    with pytest.raises(ValueError):
+        p.check()
+    with pytest.raises(ValueError):
+        oracle.chunk(np.zeros(10, np.uint8), p)
+
+
+def test_check_params_accepts_boundaries():
+    """Smallest accepted values: L = 2, min = L, max = min, T = 1, S = 0."""
+    p = oracle.Params(1, 2, 1, 0, 2, 2)
+    assert oracle.check_params_c(p) == 0
+    p.check()
+    # every chunk is exactly min = max = 2 bytes (P:266 forced cut), last one shorter
+    assert oracle.chunk(np.arange(7, dtype=np.uint8), p).tolist() == [2, 4, 6, 7]
+
+
+# ---------------------------------------------------------------- measurement: bytes the method reads
+def test_chunk_window_is_prefix_of_chunk():
+    """oracle_chunk_window stops after the first chunk starting beyond last_start
+    and otherwise equals oracle_chunk (the windowed whole-list check relies on it)."""
+    rng = np.random.default_rng(77)
+    b = rng.integers(0, 256, 300_000).astype(np.uint8)
+    p = oracle.table1(4)
+    full = oracle.chunk(b, p)
+    for last_start in (0, 1, 5000, int(full[10]), int(full[10]) + 1, b.size):
+        got, _, _ = oracle.chunk_window(b, last_start, p)
+        starts = np.concatenate([[0], full[:-1]])
+        want = full[: int(np.searchsorted(starts, last_start, side="right"))]
+        assert np.array_equal(got, want), last_start
+
+
+def test_touched_units_match_query_form():
+    """Distinct units (1, 32, 128, 512 B) holding a compared byte: the literal
+    loop's running count equals the query form's interval union (anchors P:179 /
+    d+1+S P:189, deciding pair P:225-227) on random small cases."""
+    rng = np.random.default_rng(5)
+    for it in range(250):
+        n = int(rng.integers(0, 3000))
+        b = rng.integers(0, int(rng.choice([2, 3, 4, 256])), n).astype(np.uint8)
+        L = int(rng.integers(2, 7))
+        mn = int(rng.integers(L, 200))
+        p = oracle.Params(int(rng.integers(0, 2)), L, int(rng.integers(1, 20)), int(rng.integers(0, 50)), mn,
+                          int(rng.integers(mn, 600)), pairs=bool(rng.integers(0, 2)))
+        _, pairs, t = oracle.chunk_window(b, n, p, unit_shifts=(0, 5, 7, 9))
+        assert {k: v[0] for k, v in t.items()} == oracle.touched_units_query(b, p, (0, 5, 7, 9)), it
+        _, ex = oracle.chunk(b, p, return_examined=True)
+        assert pairs == ex
+
+
+@pytest.mark.parametrize("n", [1, 100, 2044, 2045, 5000, 70_001])
+def test_touched_bytes_closed_form_constant(n):
+    """Constant data: no pair is favourable or opposing, so every
+    chunk compares pairs base+min-L .. limit-2 and is cut at limit: the
+    bytes read are [base+min-L, limit) per chunk, limit - base - min + L of them
+    (none when fewer than 2 bytes follow the anchor)."""
+    p = oracle.table1(4)
+    b = np.full(n, 9, np.uint8)
+    cuts, _, t = oracle.chunk_window(b, n, p, unit_shifts=(0,))
+    want, base = 0, 0
+    for c in cuts.tolist():
+        span = c - base - p.min_size + p.seq_length     # bytes from the anchor to the limit
+        want += span if span >= 2 else 0                 # no pair fits in fewer than 2 bytes
+        base = c
+    assert t[0][0] == want
