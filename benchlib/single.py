@@ -192,8 +192,9 @@ def run(args, w: Workload) -> int:
                    "oracle_threads": chk.get("threads"), "oracle_s": chk.get("oracle_s"),
                    "oracle_all_cores_GBps": round(w.n / chk["oracle_s"] / 1e9, 3) if chk.get("oracle_s") else None},
         "cpu_baseline": {"value": cpu1["GBps"], "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": f"first {cpu1['bytes']} bytes of the stream in 1 GiB pieces from true cuts "
-                                   f"({cpu1['seconds']} s, plain single-threaded C loop)",
+                         "sample": f"first {cpu1['bytes']} bytes of the stream in 1 GiB pieces starting at true cuts "
+                                   f"({cpu1['bytes_processed']} bytes processed incl. piece overlaps, "
+                                   f"{cpu1['seconds']} s, plain single-threaded C loop)",
                          "cpu": cpu_desc(), "host_cores": os.cpu_count()},
         "e2e": ee,
         "clocks": clocks,

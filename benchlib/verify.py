@@ -98,7 +98,7 @@ def time_oracle_single(get_bytes, n: int, p: "oracle.Params", cuts: np.ndarray, 
     """The oracle as it stands (plain single-threaded C loop, oracle.chunk) on
     consecutive pieces of the stream, each starting at a true cut, until
     ~budget_s of CPU time: GB/s = bytes / time (a bounded sample)."""
-    done, t, pos = 0, 0.0, 0
+    work, t, pos = 0, 0.0, 0
     cuts = np.ascontiguousarray(cuts, dtype=np.uint64)
     while pos < n and t < budget_s:
         end = min(n, pos + piece)
@@ -106,13 +106,15 @@ def time_oracle_single(get_bytes, n: int, p: "oracle.Params", cuts: np.ndarray, 
         t0 = time.perf_counter()
         got = oracle.chunk(buf, p)
         t += time.perf_counter() - t0
-        done += end - pos
-        # next piece starts at a cut both sides agree on (the last one that the
-        # truncated piece cannot have moved: a chunk starting >= end - max may differ)
+        work += end - pos
         if end >= n:
+            pos = n
             break
+        # the next piece starts at the last cut the truncated piece cannot have
+        # moved (a chunk starting >= end - max may differ from the stream's)
         safe = got[(got + np.uint64(pos)) <= np.uint64(end - p.max_size)]
         if safe.size == 0:
             break
         pos = pos + int(safe[-1])
-    return {"GBps": round(done / t / 1e9, 4), "bytes": done, "seconds": round(t, 2)}
+    done = pos
+    return {"GBps": round(work / t / 1e9, 4), "bytes": done, "bytes_processed": work, "seconds": round(t, 2)}
