@@ -612,6 +612,10 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_walk(Work w)
     walker_finish(wk);
 }
 
+}  // namespace seqcdc
+#include "seqcdc_lane.cuh"
+namespace seqcdc {
+
 // ------------------------------------------------------------------ 2. stitch (batches)
 template <int MODE, int MSPEC>
 __global__ void __launch_bounds__(1024) k_stitch(Work w)
@@ -933,6 +937,233 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
     }
 }
 
+// ------------------------------------------------------------------ many segments (lane walker): post in two launches
+// k_lpost (one CTA): which segments lie on the valid chain, each one's entry and
+// valid count, the exclusive scan of the counts; k_lcopy (grid): the copy.
+// A segment's extension merges into the next segment's chain except when it ran
+// through it without meeting a common cut (a "jumper": target != s+1); the
+// valid path from segment 0 only changes at jumpers, so it is followed over the
+// (few) jumpers alone: jumper j is on the path iff the path has not already
+// jumped past it; a live jumper kills the segments strictly between it and its
+// target and gives its target the entry midx[j].  Everything else is parallel.
+constexpr uint32_t LP_JCAP = 8192;                 // jumpers followed from shared memory
+constexpr uint32_t LP_MAX_SEGS = 180000;           // flags (1 B each) + jumpers fit in 227 KB
+constexpr uint32_t LP_SMEM = 4 * LP_JCAP + LP_MAX_SEGS;
+
+__device__ __forceinline__ uint32_t tgt_of(const Work &w, uint32_t i, uint32_t k)
+{
+    const int32_t t = __ldcg(w.target + i);
+    return t >= 0 ? (uint32_t)t : k;               // the stream (range) end
+}
+
+__global__ void __launch_bounds__(1024) k_lpost(Work w)
+{
+    extern __shared__ __align__(128) uint8_t sm[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // the walk complete and its writes visible
+    const uint32_t k = w.nseg1;
+    uint32_t *jl = (uint32_t *)sm;                 // [LP_JCAP] jumpers in ascending order
+    uint8_t *fl = sm + 4 * LP_JCAP;                // [k]: bit 0 dead, bit 1 entry written by a live jumper
+    __shared__ uint32_t nj_s, wsum32[32];
+    __shared__ uint64_t wsum64[32];
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, wid = tid >> 5;
+    const uint32_t per = (k + nt - 1) / nt;
+    const uint32_t b0 = min(k, tid * per), b1 = min(k, b0 + per);
+    // A. flags cleared; jumpers counted per thread, then placed in order
+    uint32_t cj = 0;
+    for (uint32_t i = b0; i < b1; i++) {
+        fl[i] = 0;
+        if (i + 1 < k && tgt_of(w, i, k) != i + 1) cj++;
+    }
+    uint32_t inc = cj;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum32[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t x = lane < (int)(nt >> 5) ? wsum32[lane] : 0;
+        uint32_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL, xi, o);
+            if (lane >= o) xi += t;
+        }
+        wsum32[lane] = xi - x;
+        if (lane == 31) nj_s = xi;
+    }
+    __syncthreads();
+    const uint32_t nj = nj_s;
+    uint32_t pos = wsum32[wid] + inc - cj;
+    if (nj <= LP_JCAP)
+        for (uint32_t i = b0; i < b1; i++)
+            if (i + 1 < k && tgt_of(w, i, k) != i + 1) jl[pos++] = i;
+    __syncthreads();
+    // B. follow the valid path over the jumpers (one warp)
+    if (wid == 0) {
+        uint32_t state = 0;                        // the next segment on the path
+        if (nj <= LP_JCAP) {
+            for (uint32_t base = 0; base < nj; base += 32) {
+                const uint32_t idx = base + lane;
+                const uint32_t j = idx < nj ? jl[idx] : FULL;
+                const uint32_t t = idx < nj ? tgt_of(w, j, k) : k;
+                uint32_t livem = 0;
+                const uint32_t m = min(32u, nj - base);
+                for (uint32_t l = 0; l < m; l++) {
+                    const uint32_t jj = __shfl_sync(FULL, j, l), tt = __shfl_sync(FULL, t, l);
+                    if (state <= jj) {             // the path reaches jumper jj: it is live
+                        state = tt;
+                        livem |= 1u << l;
+                    }
+                }
+                if ((livem >> lane) & 1u) {
+                    for (uint32_t i = j + 1; i < t && i < k; i++) fl[i] = 1;
+                    if (t < k) {
+                        fl[t] = 2;
+                        w.entry[t] = __ldcg(w.midx + j);
+                    }
+                }
+                __syncwarp();
+            }
+        } else {                                   // many jumpers: follow segment by segment
+            uint32_t cur = 0;
+            while (cur + 1 < k) {
+                const uint32_t i = cur + lane;
+                const bool pass = i + 1 < k && tgt_of(w, i, k) == i + 1;
+                const uint32_t nb = __ballot_sync(FULL, !pass);
+                if (!nb) {
+                    cur += 32;
+                    continue;
+                }
+                const uint32_t ic = cur + __ffs(nb) - 1;
+                if (ic + 1 >= k) break;
+                const uint32_t t = tgt_of(w, ic, k);
+                for (uint32_t x = ic + 1 + lane; x < t && x < k; x += 32) fl[x] = 1;
+                if (lane == 0 && t < k) {
+                    fl[t] = 2;
+                    w.entry[t] = __ldcg(w.midx + ic);
+                }
+                __syncwarp();
+                if (t >= k) break;
+                cur = t;
+            }
+        }
+    }
+    __syncthreads();
+    // C. entries and valid counts, then the exclusive scan of the counts
+    uint64_t loc = 0;
+    for (uint32_t i = b0; i < b1; i++) {
+        const uint8_t f = fl[i];
+        uint64_t c = 0;
+        int64_t e = ENTRY_DEAD;
+        if (!(f & 1u)) {
+            e = i == 0 ? -1 : ((f & 2u) ? w.entry[i] : __ldcg(w.midx + i - 1));
+            c = (__ldcg(w.Lcnt + i) & CNT_MASK) - (uint64_t)(e + 1) + __ldcg(w.Xcnt + i) + __ldcg(w.cont_cnt + i);
+        }
+        w.entry[i] = e;
+        w.seg_count[i] = c;
+        loc += c;
+    }
+    uint64_t inc64 = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(FULL, inc64, o);
+        if (lane >= o) inc64 += t;
+    }
+    if (lane == 31) wsum64[wid] = inc64;
+    __syncthreads();
+    if (wid == 0) {
+        const uint64_t x = lane < (int)(nt >> 5) ? wsum64[lane] : 0;
+        uint64_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(FULL, xi, o);
+            if (lane >= o) xi += t;
+        }
+        wsum64[lane] = xi - x;
+    }
+    __syncthreads();
+    uint64_t run = wsum64[wid] + inc64 - loc;
+    for (uint32_t i = b0; i < b1; i++) {
+        w.seg_out[i] = run;
+        run += w.seg_count[i];
+    }
+    if (tid == nt - 1) {
+        const uint64_t total = run;
+        if (w.tail_n && (fl[k - 1] & 1u)) *w.tail_n = 0;    // the last chain is not the valid one
+        if (w.summary) {                                      // the overhang = the last valid cut
+            uint64_t ov = w.out_add;
+            for (int32_t s3 = (int32_t)k - 1; s3 >= 0; s3--) {
+                if (fl[s3] & 1u) continue;
+                const int64_t e = w.entry[s3];
+                const uint64_t nc = __ldcg(w.cont_cnt + s3), nx = __ldcg(w.Xcnt + s3);
+                const uint64_t lc = __ldcg(w.Lcnt + s3) & CNT_MASK;
+                const Seg g = get_seg(w, s3);
+                if (nc) ov = __ldcg(cont_slot(w, s3, __ldcg(w.X + g.Xoff + nx - 1)) + nc - 1) + w.out_add;
+                else if (nx) ov = __ldcg(w.X + g.Xoff + nx - 1) + w.out_add;
+                else if (lc > (uint64_t)(e + 1)) ov = __ldcg(w.L + g.Loff + lc - 1) + w.out_add;
+                else continue;
+                break;
+            }
+            w.summary[0] = ov;
+            w.summary[1] = total;
+        }
+        w.cut_index[0] = 0;
+        w.cut_index[1] = total;
+        *w.ncuts = total;
+    }
+    if (w.push_blk) {                                         // fused exchange (as in k_post)
+        __syncthreads();
+        const uint64_t tn = w.tail_n ? min(*(volatile uint64_t *)w.tail_n, (uint64_t)w.tail_max) : 0;
+        for (uint32_t i = tid; i < 3 + tn; i += nt)
+            w.push_blk[i] = i == 0 ? w.summary[0] : i == 1 ? w.summary[1] : i == 2 ? tn : __ldcg(w.tail + (i - 3));
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(w.push_flag), "l"(w.push_value) : "memory");
+        }
+    }
+}
+
+// one warp per segment, 8 loads in flight per lane before their stores
+__global__ void __launch_bounds__(256) k_lcopy(Work w)
+{
+    const uint32_t k = w.nseg1;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t s2 = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s2 < k; s2 += nw) {
+        const int64_t e = __ldcg(w.entry + s2);
+        if (e == ENTRY_DEAD) continue;
+        const Seg g = get_seg(w, s2);
+        uint64_t *out = w.cuts + __ldcg(w.seg_out + s2);
+        const uint64_t lc = __ldcg(w.Lcnt + s2) & CNT_MASK, nx = __ldcg(w.Xcnt + s2), nc = __ldcg(w.cont_cnt + s2);
+        const uint64_t nl = lc - (uint64_t)(e + 1);
+        const uint64_t *Ls = w.L + g.Loff + (e + 1);
+        const uint64_t *Xs = w.X + g.Xoff;
+        const uint64_t add = w.out_add;
+#pragma unroll 1
+        for (uint64_t i0 = 0; i0 < nl + nx; i0 += 256) {
+            uint64_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint64_t i = i0 + 32 * u + lane;
+                v[u] = i < nl ? __ldcg(Ls + i) : (i < nl + nx ? __ldcg(Xs + (i - nl)) : 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint64_t i = i0 + 32 * u + lane;
+                if (i < nl + nx) out[i] = v[u] + add;
+            }
+        }
+        if (nc) {
+            const uint64_t *Cs = cont_slot(w, s2, __ldcg(Xs + nx - 1));
+            for (uint64_t i = lane; i < nc; i += 32) out[nl + nx + i] = __ldcg(Cs + i) + add;
+        }
+    }
+}
+
 // an empty range's exchange block (no walk ran): [overhang, 0, 0] + flag
 __global__ void k_push_empty(uint64_t *blk, uint64_t *flag, uint64_t ov, uint64_t value)
 {
@@ -964,9 +1195,9 @@ struct Plan {
     size_t o_ctrl, o_Lcnt, o_str_first, o_cont_cnt, o_seg_lo, o_seg_hi, o_seg_stream, o_Loff, o_Xoff,
         o_Lcap, o_Xcap, o_Xcnt, o_target, o_midx, o_entry, o_seg_count, o_seg_out, o_L, o_X, o_FB;
     uint32_t walk_grid;
+    bool lane;             // single stream on the lane walker (k_lwalk + k_lpost + k_lcopy)
 };
 
-static int g_sms = 0;
 static std::atomic<uint64_t> g_launches{0};   // kernels this library has launched (process-wide)
 static uint64_t g_force_G = 0;
 static std::mutex g_mu;
@@ -980,7 +1211,6 @@ static void set_attrs()
 {
     cudaFuncSetAttribute((const void *)k_stitch<MODE, MSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          STITCH_SMEM);
-    cudaFuncSetAttribute((const void *)k_post, cudaFuncAttributeMaxDynamicSharedMemorySize, 20 * STITCH_MAX_SEGS);
 }
 
 template <int MODE>
@@ -997,10 +1227,7 @@ static int env_int(const char *name, int dflt)
     return e ? atoi(e) : dflt;
 }
 
-// Ring geometry for a parameter set: the prefetch must reach past the
-// sub-minimum region plus about two examined windows, so that a chunk
-// step does not wait a full HBM round trip.  Blocks grow with min_size so the
-// slot count stays <= 8.
+// Ring geometry of the warp walker (fixed in this build; reported by build_info).
 static void ring_geometry(const seqcdc_params_t *, DevParams &d)
 {
     d.bs = BLK_SHIFT;
@@ -1008,45 +1235,74 @@ static void ring_geometry(const seqcdc_params_t *, DevParams &d)
     d.ah = AHEAD;
 }
 
-static int g_occ_by_smem[66];
+// Per device: SM count, occupancies, and the function attributes (dynamic
+// shared memory opt-ins are per device context, so they are set once for every
+// device a process uses).
+struct DevInfo {
+    int sms = 0;
+    int occ_warp = 0;      // warp-walker CTAs (one warp each) per SM
+    int occ_lane = 0;      // lane-walker CTAs per SM
+};
+static DevInfo g_dev[64];
 static int g_last_occ;
 
-static int device_info(int &sms, int &occ, uint32_t smem = 0)
+static int device_info(int &sms, int &occ, int *occ_lane = nullptr)
 {
+    int dev;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SEQCDC_ECUDA;
     std::lock_guard<std::mutex> lk(g_mu);
-    if (!g_sms) {
-        int dev;
-        if (cudaGetDevice(&dev) != cudaSuccess) return SEQCDC_ECUDA;
+    DevInfo &d = g_dev[dev];
+    if (!d.sms) {
         int nsm = 0;
         if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return SEQCDC_ECUDA;
         set_attrs_mode<0>();
         set_attrs_mode<1>();
         set_attrs_mode<2>();
         set_attrs_mode<3>();
-        g_sms = nsm;
-    }
-    const uint32_t key = std::min<uint32_t>(smem / 1024, 65);
-    if (!g_occ_by_smem[key]) {
-        int occ_ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_, k_walk<0, 4, true>, 32, smem) != cudaSuccess)
+        cudaFuncSetAttribute((const void *)k_post, cudaFuncAttributeMaxDynamicSharedMemorySize, STITCH_SMEM);
+        cudaFuncSetAttribute((const void *)k_lpost, cudaFuncAttributeMaxDynamicSharedMemorySize, LP_SMEM);
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_walk<0, 4, true>, 32, 0) != cudaSuccess)
             return SEQCDC_ECUDA;
         // 24 walkers per SM measured best (25 -- the smem limit -- leaves almost no L1
         // and runs ~25% slower on config 2; profiles/r01/sweeps.md)
-        if (occ_ > 24) occ_ = 24;
-        const int v = env_int("SEQCDC_WALKERS_PER_SM", 0);
-        if (v > 0 && v < occ_) occ_ = v;
-        g_occ_by_smem[key] = occ_ > 0 ? occ_ : 1;
+        d.occ_warp = std::max(1, std::min(o, 24));
+        int ol = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ol, k_lwalk<0, true>, lw::THREADS, 0) != cudaSuccess)
+            return SEQCDC_ECUDA;
+        d.occ_lane = std::max(1, ol);
+        d.sms = nsm;
     }
-    sms = g_sms;
-    occ = g_occ_by_smem[key];
+    sms = d.sms;
+    occ = d.occ_warp;
+    const int v = env_int("SEQCDC_WALKERS_PER_SM", 0);
+    if (v > 0 && v < occ) occ = v;
+    if (occ_lane) *occ_lane = d.occ_lane;
     return SEQCDC_OK;
+}
+
+// Which walker a single-stream call uses: the lane walker (skip-aware sparse
+// reads) for long streams with M <= 4 favourable pairs per run (every Table I
+// row), the warp walker otherwise.  SEQCDC_WALKER=warp|lane forces one (tests).
+static bool use_lane_walker(uint64_t total, const seqcdc_params_t *p, bool single)
+{
+    if (!single) return false;
+    const uint32_t M = p->seq_length - ((p->flags & SEQCDC_FLAG_PAIRS) ? 0u : 1u);
+    if (M > 4) return false;
+    const char *e = getenv("SEQCDC_WALKER");
+    if (e && !strcmp(e, "warp")) return false;
+    if (e && !strcmp(e, "lane")) return true;
+    // off by default until it beats the warp walker (profiles/r02/lane_walker.md)
+    const int mib = env_int("SEQCDC_LW_MIN_MIB", -1);
+    return mib >= 0 && total >= ((uint64_t)mib << 20);
 }
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int sms, int occ, Plan &pl,
-                      bool single, uint64_t stop, bool short_tail = false)
+                      bool single, uint64_t stop, bool short_tail = false, int occ_lane = 0)
 {
+    pl.lane = occ_lane > 0;
     // up to ~1.5 GiB the run ends with the longest seam extension, and 22 walkers
     // per SM (longer segments, less contention on the tail) measured ~4% faster
     // than 24 on config 2; larger inputs are throughput-bound (profiles/r01/sweeps.md)
@@ -1067,6 +1323,15 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     denom = std::max<uint64_t>(1, denom * spw / 100);
     uint64_t G = (total + denom - 1) / denom;
     G = std::max<uint64_t>(G, floor_chunks * mx);
+    if (pl.lane) {
+        // lane walker: one segment per lane, all lanes resident at once; the floor
+        // keeps a segment several merge distances long (SURVEY.md [MC-3])
+        const uint64_t ctas = (uint64_t)std::max(1, std::min(occ_lane, env_int("SEQCDC_LW_CTAS_PER_SM", 4)));
+        const uint64_t lanes = (uint64_t)sms * ctas * lw::THREADS;
+        G = std::max<uint64_t>((total + lanes - 1) / lanes,
+                               (uint64_t)std::max(1, env_int("SEQCDC_LW_G_FLOOR_CHUNKS", 24)) * mx);
+        G = std::max<uint64_t>(G, (total + LP_MAX_SEGS - 3) / (LP_MAX_SEGS - 2));
+    }
     if (g_force_G) G = std::max<uint64_t>(g_force_G, mx);
     G = std::min<uint64_t>(G, std::max<uint64_t>(G_CEIL, mx));
     G = (G + mx - 1) / mx * mx;
@@ -1095,6 +1360,7 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     }
     pl.FB_items = total / mn + ns + pl.nseg_max + 2;
     pl.walk_grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(pl.nseg_max, walkers));
+    if (pl.lane) pl.walk_grid = (uint32_t)((pl.nseg1 + lw::THREADS - 1) / lw::THREADS);
     size_t o = 0;
     auto take = [&](size_t bytes) {
         size_t r = o;
@@ -1159,9 +1425,43 @@ static void prof_mark(ProfRec *r, int i, cudaStream_t st)
     if (r) cudaEventRecord(r->e[i], st);
 }
 
+static void launch_pdl(const void *fn, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, const Work &w)
+{
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void *args[] = {(void *)&w};
+    cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+template <int MODE>
+static void launch_lane(const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
+{
+    prof_mark(pr, 1, st);
+    if (w.p.M == 4) k_lwalk<MODE, true><<<pl.walk_grid, lw::THREADS, 0, st>>>(w);
+    else k_lwalk<MODE, false><<<pl.walk_grid, lw::THREADS, 0, st>>>(w);
+    prof_mark(pr, 2, st);
+    // k_lpost waits on the device (griddepcontrol.wait) for the walk: launched early
+    launch_pdl((const void *)k_lpost, dim3(1), dim3(1024), 4 * LP_JCAP + pl.nseg1, st, pr == nullptr, w);
+    k_lcopy<<<std::max(1, sms * 8), 256, 0, st>>>(w);
+    g_launches += 3;
+}
+
 template <int MODE, int MSPEC>
 static void launch_all(const Work &w, const Plan &pl, int sms, cudaStream_t st, ProfRec *pr)
 {
+    if (pl.lane) {
+        launch_lane<MODE>(w, pl, sms, st, pr);
+        return;
+    }
     prof_mark(pr, 1, st);
     if (w.single) k_walk<MODE, MSPEC, true><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
     else k_walk<MODE, MSPEC, false><<<pl.walk_grid, 32, walker_smem(w.p), st>>>(w);
@@ -1215,7 +1515,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
                bool single, const TailReq &tail)
 {
     if (ws_bytes < pl.bytes) return SEQCDC_ENOMEM;
-    if (total / pl.G + 2 > STITCH_MAX_SEGS) return SEQCDC_EINVAL;  // one stream's segments fit the stitch smem
+    if (total / pl.G + 2 > (pl.lane ? LP_MAX_SEGS : STITCH_MAX_SEGS)) return SEQCDC_EINVAL;  // post smem limits
     Work w;
     memset(&w, 0, sizeof(w));
     w.in = d_in;
@@ -1313,12 +1613,13 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
 {
     DevParams geo;
     ring_geometry(p, geo);
-    int sms, occ;
-    int rc = device_info(sms, occ, walker_smem(geo));
+    int sms, occ, occ_lane;
+    int rc = device_info(sms, occ, &occ_lane);
     if (rc) return rc;
     g_last_occ = occ;
     Plan pl;
-    make_plan(total, ns, p, sms, occ, pl, single_api, stop, tail.max > 0);
+    const bool lane = use_lane_walker(total, p, single_api);
+    make_plan(total, ns, p, sms, occ, pl, single_api, stop, tail.max > 0, lane ? occ_lane : 0);
     const size_t extra = single_api ? SINGLE_EXTRA : 0;
     uint8_t *ws = (uint8_t *)d_ws;
     bool owned = false;
@@ -1411,18 +1712,19 @@ SEQCDC_API size_t seqcdc_workspace_size(uint64_t total, uint32_t ns, const seqcd
     if (seqcdc_validate_params(p)) return 0;
     DevParams geo;
     ring_geometry(p, geo);
-    int sms, occ;
-    if (device_info(sms, occ, walker_smem(geo))) {   // no device: an upper bound (32 CTAs/SM)
+    int sms, occ, occ_lane;
+    if (device_info(sms, occ, &occ_lane)) {   // no device: an upper bound (32 CTAs/SM)
         sms = 148;
         occ = 32;
+        occ_lane = 8;
     }
-    Plan pl;
-    Plan pb;
-    Plan pt;
+    Plan pl, pb, pt, ql, qt;
     make_plan(total, ns ? ns : 1, p, sms, occ, pl, ns <= 1, total);
     make_plan(total, ns ? ns : 1, p, sms, occ, pb, false, total);
     make_plan(total, 1, p, sms, occ, pt, true, total, true);
-    return std::max(std::max(pl.bytes, pb.bytes), pt.bytes) + SINGLE_EXTRA;
+    make_plan(total, 1, p, sms, occ, ql, true, total, false, occ_lane);
+    make_plan(total, 1, p, sms, occ, qt, true, total, true, occ_lane);
+    return std::max({pl.bytes, pb.bytes, pt.bytes, ql.bytes, qt.bytes}) + SINGLE_EXTRA;
 }
 
 SEQCDC_API int seqcdc_chunk_batch(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint64_t total,
@@ -1690,15 +1992,25 @@ SEQCDC_API const char *seqcdc_strerror(int code)
 SEQCDC_API const char *seqcdc_build_info(void)
 {
     static char buf[256];
-    int sms = 0, occ = 0;
-    device_info(sms, occ);
+    int sms = 0, occ = 0, ol = 0;
+    device_info(sms, occ, &ol);
     snprintf(buf, sizeof(buf),
-             "seqcdc sm_100a cp.async ring blk=%u nblk=%u ahead=%u walkers=%dx%d (last call); win_pairs=%u k_ext=%u",
-             BLK, NBLK, AHEAD, sms, g_last_occ, WIN_PAIRS, K_EXT);
+             "seqcdc sm_100a warp walker: cp.async ring blk=%u nblk=%u ahead=%u walkers=%dx%d (last call), "
+             "win_pairs=%u; lane walker: %u-B bulk-copy lines x2, %u-thread CTAs, %d/SM max, pf=%u; k_ext=%u",
+             BLK, NBLK, AHEAD, sms, g_last_occ, WIN_PAIRS, lw::LINE, lw::THREADS, ol, (unsigned)SEQCDC_LW_PF, K_EXT);
     return buf;
 }
 
 #ifdef SEQCDC_TIMELINE
+SEQCDC_API int seqcdc_debug_lw_stats(uint64_t *out4, int reset)
+{
+    if (reset) {
+        uint64_t z[4] = {0, 0, 0, 0};
+        return cudaMemcpyToSymbol(lw::g_lw_stats, z, sizeof(z)) == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
+    }
+    return cudaMemcpyFromSymbol(out4, lw::g_lw_stats, sizeof(uint64_t) * 4) == cudaSuccess ? SEQCDC_OK : SEQCDC_ECUDA;
+}
+
 SEQCDC_API int seqcdc_debug_timeline(uint64_t *d_buf, uint64_t nseg_cap)
 {
     if (cudaMemcpyToSymbol(g_tl, &d_buf, sizeof(d_buf)) != cudaSuccess) return SEQCDC_ECUDA;

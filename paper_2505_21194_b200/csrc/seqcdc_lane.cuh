@@ -1,0 +1,501 @@
+// seqcdc_lane.cuh -- the per-lane, skip-aware SeqCDC walker (SURVEY.md 8(f)
+// NEXT-2 made the hot path for long streams).  Included by seqcdc.cu after the
+// segment helpers (Work, Seg, get_seg, seg_start, fix_overflows).
+//
+// Why: the method itself never reads the sub-minimum region of a chunk
+// nor the bytes a content-defined skip jumps over; on config 5
+// it compares bytes in only 3.8% of the stream's 32-B sectors.  The warp
+// walker streams every byte through shared memory and is therefore bound by
+// HBM at ~n / 6.6 TB/s.  Here every LANE owns one speculative chain (one
+// segment) and fetches only the 128-B lines its scan touches, with 1-D bulk
+// copies (TMA, cp.async.bulk) into two private line slots, each completing on
+// its own mbarrier.  A lane whose line has not landed simply skips that loop
+// iteration (mbarrier.test_wait, no blocking), so the warp keeps scanning for
+// the lanes whose data is there; thousands of chains per SM hide the HBM
+// latency of the dependent chunk-to-chunk jumps.
+//
+// One loop iteration of a lane examines one 16-byte group: 16 byte pairs
+// (bytes q..q+16), classified with SIMD-in-word compares (4 pairs per 32-bit
+// word), the favourable-run mask by funnel-shift AND with the
+// previous group's flags, the opposing count by popc and the
+// SkipTrigger-th opposing pair by a SWAR byte select.  Decision in
+// pair order: run end first -> cut; T-th opposing pair first -> skip
+// to d+1+S with fresh counters (reading c3); neither -> next group; past
+// the limit -> forced cut.
+//
+// Segment protocol (same lists as the warp walker, so the post kernels are
+// shared): the lane records its speculative cuts < segment end in L_s and
+// publishes the count with release semantics ONCE, when the speculative part
+// is complete (DONE).  Its extension then walks on, checking each cut against
+// the DONE list of the chain owning that region (a cut not yet decidable is
+// simply walked past: after a merge both chains are identical, so any later
+// common cut is a merge too).
+#pragma once
+
+namespace seqcdc {
+namespace lw {
+
+#ifndef SEQCDC_LW_LINE_SHIFT
+#define SEQCDC_LW_LINE_SHIFT 7
+#endif
+#ifndef SEQCDC_LW_WARPS
+#define SEQCDC_LW_WARPS 4
+#endif
+#ifndef SEQCDC_LW_PF
+#define SEQCDC_LW_PF 64        // prefetch the next line once the scan is this far into a line
+#endif
+
+constexpr uint32_t LSH = SEQCDC_LW_LINE_SHIFT;
+constexpr uint32_t LINE = 1u << LSH;                 // bytes per bulk copy / slot
+constexpr uint32_t LMASK = LINE - 1;
+constexpr uint32_t STRIDE = 2 * LINE + 16;           // per lane: 2 slots + 16 B of padding; 16 B mod 128 B keeps
+                                                     // the 8 lanes of each LDS.128 phase on distinct banks
+constexpr uint32_t WARPS = SEQCDC_LW_WARPS;
+constexpr uint32_t THREADS = 32 * WARPS;
+constexpr uint32_t SMEM = THREADS * STRIDE;
+static_assert(32 * STRIDE >= RING, "a finished warp's lane slots host the fallback walker's ring");
+static_assert(SMEM <= 48 * 1024, "static shared memory");
+static_assert(SEQCDC_LW_PF % 16 == 0 && SEQCDC_LW_PF < (int)LINE, "prefetch point inside a line");
+
+enum { PH_SPEC = 0, PH_EXT = 1, PH_TAIL = 2, PH_DONE = 3 };
+#ifdef SEQCDC_TIMELINE
+__device__ unsigned long long g_lw_stats[4];   // warp steps, groups scanned, fills issued
+#endif
+
+#ifdef SEQCDC_TIMELINE
+// per segment: globaltimer at start / end of the speculative part / end, and
+// (speculative cuts << 32 | extension cuts)  (tools/lane_timeline.py)
+__device__ __forceinline__ void tl_lane(uint32_t s, int k, uint64_t v = 0)
+{
+    if (g_tl && s < g_tl_cap) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_tl[4 * s + k] = k == 3 ? v : t;
+    }
+}
+#define TL_LANE(s, k, v) tl_lane((s), (k), (v))
+#else
+#define TL_LANE(s, k, v)
+#endif
+constexpr uint32_t NONE = 0xffffffffu;
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ uint4 lds128(uint32_t addr)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
+// ------------------------------------------------------------------ the lane's byte source
+// Two slots of one LINE each.  A slot holds (or is being filled with) one
+// LINE-aligned line of the job, tagged by its line number.  Fills are 16-byte
+// cp.async copies; every loop step the warp commits one cp.async group and
+// waits until at most LAG groups are in flight, so a fill issued in step t is
+// complete from step t + 1 + LAG on (`rdy`): no barrier, no polling, and the
+// warp only blocks if a fill is older than LAG steps and still not landed.
+#ifndef SEQCDC_LW_LAG
+#define SEQCDC_LW_LAG 2
+#endif
+constexpr uint32_t LAG = SEQCDC_LW_LAG;
+
+struct Src {
+    uint64_t rb;         // absolute address of relative position 0 (LINE-aligned)
+    uint32_t lo_rel;     // first byte of the job (relative)
+    uint32_t end_rel;    // end of the loadable data (relative, clamped)
+    uint32_t sb;         // shared address of this lane's region
+    uint32_t tag0, tag1; // line held by each slot (NONE: none)
+    uint32_t rdy0, rdy1; // first step at which the slot's fill is complete
+};
+
+// Start filling slot k with line `ln` in step `step` (the slot's previous fill is complete).
+__device__ __forceinline__ void fill(Src &s, uint32_t k, uint32_t ln, uint32_t step)
+{
+    const uint32_t dst = s.sb + k * LINE;
+    const uint32_t x0 = ln << LSH;
+    uint32_t r = step + 1 + LAG;
+    if (x0 >= s.lo_rel && x0 + LINE <= s.end_rel) {
+        const uint64_t src = s.rb + x0;
+#pragma unroll
+        for (uint32_t i = 0; i < LINE; i += 16) cp_async16(dst + i, src + i);
+    } else {
+        // a line at the edge of the data: copy the bytes that exist, one by one
+#pragma unroll 1
+        for (uint32_t i = 0; i < LINE; i++) {
+            const uint32_t x = x0 + i;
+            if (x >= s.lo_rel && x < s.end_rel) sts8(dst + i, *(const volatile uint8_t *)(s.rb + x));
+        }
+        r = step;
+    }
+#ifdef SEQCDC_TIMELINE
+    atomicAdd(&g_lw_stats[2], 1ull);
+#endif
+    if (k) {
+        s.tag1 = ln;
+        s.rdy1 = r;
+    } else {
+        s.tag0 = ln;
+        s.rdy0 = r;
+    }
+}
+
+// Line l lives in slot l & 1, so the two slots always hold consecutive lines
+// and a byte's shared address is just base + (x mod 2 LINE).
+__device__ __forceinline__ bool has(const Src &s, uint32_t ln) { return ((ln & 1u) ? s.tag1 : s.tag0) == ln; }
+
+// Is line ln resident and complete in step `step`?
+__device__ __forceinline__ bool ready(const Src &s, uint32_t ln, uint32_t step)
+{
+    return (ln & 1u) ? (s.tag1 == ln && step >= s.rdy1) : (s.tag0 == ln && step >= s.rdy0);
+}
+
+// Start filling line ln into its slot unless the slot's earlier fill is still in flight.
+__device__ __forceinline__ void request(Src &s, uint32_t ln, uint32_t step)
+{
+    if (step >= ((ln & 1u) ? s.rdy1 : s.rdy0)) fill(s, ln & 1u, ln, step);
+}
+
+__device__ __forceinline__ uint32_t slot_addr(const Src &s, uint32_t x) { return s.sb + (x & (2 * LINE - 1)); }
+
+// ------------------------------------------------------------------ one lane's chain state
+struct Chain {
+    uint32_t base, q, lim2, limit, need, carry, la;   // chunk start, group, limits, counters
+    uint32_t ph;
+    uint32_t hi_rel, stop_rel, ext_end;
+    uint64_t off;                                     // relative position -> offset into `in`
+    uint64_t *list;                                   // L_s, X_s or the tail list (by phase)
+    uint32_t n, cap;                                  // entries in `list`, its capacity
+    uint32_t nL;                                      // final count of L_s
+    // extension: segment owning the current cut, its list and a cursor into it
+    uint32_t t, j;
+    bool fresh;                                       // cursor not yet set up for segment t
+    uint64_t t_next, t_lo, t_Loff, t_word, cand;
+};
+
+// Set up the scan of the chunk starting at `base` (relative); false when the
+// chunk is decided without examining any pair (cut = limit).
+__device__ __forceinline__ bool chunk_begin(Chain &c, const Src &s, const DevParams &p, uint32_t base)
+{
+    c.base = base;
+    c.limit = base + p.mx < s.end_rel ? base + p.mx : s.end_rel;     // P:266 / stream end (c9)
+    c.lim2 = c.limit - 2;
+    const uint32_t a = base + p.mnL;
+    if (c.limit - base < 2 || a > c.lim2) return false;
+    c.need = p.T;
+    c.carry = 0;
+    c.q = a & ~15u;
+    c.la = a & 15u;
+    return true;
+}
+
+// Scan the 16-pair group at c.q (resident).  Returns the cut, or NONE when the
+// chunk continues (skip or next group; c updated).
+template <int MODE, bool M4>
+__device__ __forceinline__ uint32_t scan_group(Chain &c, const Src &s, const DevParams &p)
+{
+    constexpr uint32_t XM = (MODE & 2) ? H : 0u;                      // signed reading: flip bit 7
+    const uint32_t q = c.q;
+    const uint4 v = lds128(slot_addr(s, q));
+    const uint32_t x4 = (q + 16 <= c.lim2 + 1) ? lds32(slot_addr(s, q + 16)) : 0u;
+    uint32_t xw[5] = {v.x ^ XM, v.y ^ XM, v.z ^ XM, v.w ^ XM, x4 ^ XM};
+    uint32_t F[4], O[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint32_t y = __funnelshift_r(xw[k], xw[k + 1], 8);        // y_b = byte q+4k+b+1
+        uint32_t lt, gt;
+        lt_gt_flags(xw[k], y, lt, gt);
+        // pairs below the anchor (first group of a chunk / after a skip) are not examined
+        const uint32_t sh = (uint32_t)max((int)(8u * c.la) - 32 * k, 0);
+        uint32_t m;
+        asm("shl.b32 %0, %1, %2;" : "=r"(m) : "r"(H), "r"(sh));        // shift >= 32 -> 0
+        F[k] = ((MODE & 1) == 0 ? lt : gt) & m;
+        O[k] = ((MODE & 1) == 0 ? gt : lt) & m;
+    }
+    uint32_t R[4];
+    uint32_t prev = c.carry;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        if (M4) {
+            R[k] = F[k] & __funnelshift_l(prev, F[k], 8) & __funnelshift_l(prev, F[k], 16) &
+                   __funnelshift_l(prev, F[k], 24);
+        } else {
+            uint32_t r = F[k];
+            if (p.M > 1) r &= __funnelshift_l(prev, F[k], 8);
+            if (p.M > 2) r &= __funnelshift_l(prev, F[k], 16);
+            if (p.M > 3) r &= __funnelshift_l(prev, F[k], 24);
+            R[k] = r;
+        }
+        prev = F[k];
+    }
+    const uint32_t c0 = __popc(O[0]), c1 = __popc(O[1]), c2 = __popc(O[2]), c3 = __popc(O[3]);
+    const uint32_t ctot = c0 + c1 + c2 + c3;
+    if (((R[0] | R[1]) | (R[2] | R[3])) == 0 && ctot < c.need) {     // nothing decided in this group
+        c.need -= ctot;
+        c.carry = F[3];
+        c.la = 0;
+        c.q = q + 16;
+        return q + 16 > c.lim2 ? c.limit : NONE;                      // every pair up to the limit examined
+    }
+    // first run end (pair index in the group)
+    uint32_t r = NONE;
+#pragma unroll
+    for (int k = 3; k >= 0; k--)
+        if (R[k]) r = 4u * k + ((uint32_t)(__ffs(R[k]) - 1) >> 3);
+    // the need-th opposing pair
+    uint32_t d = NONE;
+    if (ctot >= c.need) {
+        const uint32_t e1 = c0, e2 = c0 + c1, e3 = c0 + c1 + c2;
+        const uint32_t k = c.need <= e1 ? 0u : (c.need <= e2 ? 1u : (c.need <= e3 ? 2u : 3u));
+        const uint32_t ex = k == 0 ? 0u : (k == 1 ? e1 : (k == 2 ? e2 : e3));
+        const uint32_t Ok = k == 0 ? O[0] : (k == 1 ? O[1] : (k == 2 ? O[2] : O[3]));
+        const uint32_t pc = (Ok >> 7) * 0x01010101u;
+        const uint32_t ge = ((pc | H) - (c.need - ex) * 0x01010101u) & 0x00808080u;
+        d = 4u * k + 3u - __popc(ge);
+    }
+    if (r < d) {                                                      // the run completes first
+        const uint32_t pr = q + r;
+        return pr <= c.lim2 ? pr + 2 : c.limit;
+    }
+    const uint32_t pd = q + d;                                        // the need-th opposing pair: skip
+    if (pd > c.lim2 || p.S >= c.lim2 - pd) return c.limit;           // lands past the limit (c8)
+    const uint32_t a = pd + 1 + p.S;                                  // reading c3
+    c.need = p.T;
+    c.carry = 0;
+    c.q = a & ~15u;
+    c.la = a & 15u;
+    return NONE;
+}
+
+// A cut of lane s's chain at relative position `cut`: record it where the
+// phase says (speculative list, extension list with the merge check, or the
+// range tail) and decide whether the chain goes on.  Returns false when the
+// lane's work is done (its results are written).
+__device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, const Seg &g, uint32_t s,
+                                       uint64_t stop_abs, uint32_t cut)
+{
+    const uint64_t cabs = c.off + cut;
+    if (c.ph == PH_SPEC && cut >= c.hi_rel) {          // first cut past the segment: the extension starts
+        TL_LANE(s, 1, 0);
+        st_release_u64(w.Lcnt + s, (uint64_t)c.n | DONE_BIT);
+        c.nL = c.n;
+        c.ph = PH_EXT;
+        c.list = w.X + g.Xoff;
+        c.cap = g.Xcap;
+        c.n = 0;
+        c.t = s;
+        c.t_next = seg_start(w, g, s + 1);
+        c.fresh = true;
+    }
+    if (c.ph == PH_SPEC) {
+        c.list[c.n++] = cabs;
+        if (cut < c.stop_rel) return true;
+        // the stream's (range's) last chunk
+        st_release_u64(w.Lcnt + s, (uint64_t)c.n | DONE_BIT);
+        w.Xcnt[s] = 0;
+        w.target[s] = TGT_END;
+        w.midx[s] = -1;
+        w.cont_cnt[s] = 0;
+        if (!(w.single && w.tail_max)) {
+            c.ph = PH_DONE;
+            return false;
+        }
+        // range call: the chain continues past the overhang (the next rank's merge)
+        c.ph = PH_TAIL;
+        c.list = w.tail;
+        c.n = 0;
+        bool more = false;
+        if (cut < src.end_rel) {
+            c.list[c.n++] = cabs + w.out_add;
+            more = c.n < w.tail_max && cut + w.p.mx <= src.end_rel;
+        }
+        if (!more) {
+            *w.tail_n = c.n;
+            c.ph = PH_DONE;
+        }
+        return more;
+    }
+    if (c.ph == PH_TAIL) {
+        c.list[c.n++] = cabs + w.out_add;
+        if (c.n < w.tail_max && cut + w.p.mx <= src.end_rel) return true;
+        *w.tail_n = c.n;
+        c.ph = PH_DONE;
+        return false;
+    }
+    // PH_EXT
+    int32_t tgt = TGT_OVERFLOW;
+    int64_t mi = -1;
+    if (c.n < c.cap && cut <= c.ext_end) {             // else: extension budget exhausted (phase-locked data)
+        c.list[c.n++] = cabs;
+        if (cabs >= stop_abs) {
+            tgt = TGT_END;
+        } else {
+            bool moved = c.fresh;
+#pragma unroll 1
+            while (cabs >= c.t_next) {                 // segments are uniform within a stream
+                c.t++;
+                c.t_next += w.G;
+                moved = true;
+            }
+            if (moved) {
+                c.fresh = false;
+                c.t_lo = seg_start(w, g, c.t);
+                c.t_Loff = w.single ? (uint64_t)c.t * w.capL1 : w.Loff[c.t];
+                c.t_word = 0;
+                c.j = 0;
+                c.cand = ~0ull;
+            }
+            if (cabs == c.t_lo) {                      // the owning chain's implicit first cut
+                tgt = (int32_t)c.t;
+            } else {
+                if (!(c.t_word & DONE_BIT)) {
+                    c.t_word = ld_acquire_u64(w.Lcnt + c.t);
+                    if ((c.t_word & DONE_BIT) && (c.t_word & CNT_MASK)) c.cand = __ldcg(w.L + c.t_Loff + c.j);
+                }
+                if (!(c.t_word & DONE_BIT)) return true;   // not decidable yet: walk on
+                const uint32_t cnt = (uint32_t)(c.t_word & CNT_MASK);
+#pragma unroll 1
+                while (c.cand < cabs && c.j + 1 < cnt) {
+                    c.j++;
+                    c.cand = __ldcg(w.L + c.t_Loff + c.j);
+                }
+                if (c.cand != cabs) return true;        // not a cut of the owning chain: walk on
+                tgt = (int32_t)c.t;
+                mi = (int64_t)c.j;
+            }
+        }
+    }
+    w.Xcnt[s] = c.n;
+    w.target[s] = tgt;
+    w.midx[s] = mi;
+    w.cont_cnt[s] = 0;
+    if (tgt == TGT_OVERFLOW) atomicOr(w.ctrl + C_OVF, 1u);
+    c.ph = PH_DONE;
+    TL_LANE(s, 2, 0);
+    TL_LANE(s, 3, ((uint64_t)c.nL << 32) | c.n);
+    return false;
+}
+
+
+}  // namespace lw
+
+// The per-lane walker kernel.  One segment per lane (grid = segments / THREADS).
+template <int MODE, bool M4>
+__global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
+{
+    using namespace lw;
+    __shared__ __align__(128) uint8_t sm[SMEM];
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int lane = threadIdx.x & 31;
+    const uint32_t nseg = w.ctrl[C_BAD] ? 0u : nseg_total(w);
+    const uint32_t s = blockIdx.x * THREADS + threadIdx.x;
+    const uint64_t abase = (uint64_t)(uintptr_t)w.in;
+    const DevParams p = w.p;
+
+    Src src;
+    {
+        uint32_t sb = smem_u32(sm) + threadIdx.x * STRIDE;
+        asm volatile("mov.b32 %0, %0;" : "+r"(sb));
+        src.sb = sb;
+    }
+    src.tag0 = src.tag1 = NONE;
+    src.rdy0 = src.rdy1 = 0;
+
+    Chain c;
+    c.ph = PH_DONE;
+    Seg g;
+    uint64_t stop_abs = 0;
+    uint32_t pend = NONE;                             // a cut decided without examining any pair
+    if (s < nseg) {
+        g = get_seg(w, s);
+        src.rb = (abase + g.lo) & ~(uint64_t)LMASK;
+        src.lo_rel = (uint32_t)(abase + g.lo - src.rb);
+        const uint64_t e = g.E > g.lo ? abase + g.E - src.rb : src.lo_rel;
+        src.end_rel = e > REL_CLAMP ? REL_CLAMP : (uint32_t)e;
+        c.off = src.rb - abase;
+        c.hi_rel = g.last ? FULL : src.lo_rel + (uint32_t)(g.hi - g.lo);
+        stop_abs = w.single ? w.stop : g.E;
+        c.stop_rel = stop_abs - c.off < (uint64_t)FULL ? (uint32_t)(stop_abs - c.off) : FULL;
+        c.ext_end = c.hi_rel + (uint32_t)(K_EXT * w.G);
+        c.list = w.L + g.Loff;
+        c.cap = g.Lcap;
+        c.n = 0;
+        TL_LANE(s, 0, 0);
+        if (src.lo_rel < src.end_rel) {
+            c.ph = PH_SPEC;
+            if (!chunk_begin(c, src, p, src.lo_rel)) pend = c.limit;
+        } else {                                      // an empty segment (empty stream)
+            st_release_u64(w.Lcnt + s, DONE_BIT);
+            w.Xcnt[s] = 0;
+            w.target[s] = TGT_END;
+            w.midx[s] = -1;
+            w.cont_cnt[s] = 0;
+            if (w.single && w.tail_max && g.last) *w.tail_n = 0;
+        }
+    }
+
+    // One step of every lane per iteration, in lockstep: examine one group if
+    // its lines are complete, handle a cut, keep the next lines on their way.
+    uint32_t step = 0;
+#pragma unroll 1
+    while (__any_sync(FULL, c.ph != PH_DONE)) {
+        cp_async_commit();
+        cp_async_wait<LAG>();
+        step++;
+        if (c.ph == PH_DONE) continue;
+        uint32_t cut = pend;
+        pend = NONE;
+        if (cut == NONE) {
+            const uint32_t l0 = c.q >> LSH;
+            // byte q+16 lies in the next line only for the line's last group
+            const bool two = (c.q & LMASK) == LINE - 16 && c.q + 16 <= c.lim2 + 1;
+            if (ready(src, l0, step) && (!two || ready(src, l0 + 1, step))) {
+                cut = scan_group<MODE, M4>(c, src, p);
+#ifdef SEQCDC_TIMELINE
+                atomicAdd(&g_lw_stats[1], 1ull);
+#endif
+            }
+        }
+        if (cut != NONE) {
+            if (c.ph == PH_SPEC && cut < c.hi_rel && cut < c.stop_rel) {   // the common case
+                c.list[c.n++] = c.off + cut;
+                if (!chunk_begin(c, src, p, cut)) pend = c.limit;
+            } else if (on_cut(w, c, src, g, s, stop_abs, cut)) {
+                if (!chunk_begin(c, src, p, cut)) pend = c.limit;
+            }
+        }
+        if (c.ph != PH_DONE && pend == NONE) {          // the lines the next groups need, on their way
+            const uint32_t l0 = c.q >> LSH;
+            if (!has(src, l0)) {
+                request(src, l0, step);
+            } else if ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) && ((l0 + 1) << LSH) < src.end_rel) {
+                request(src, l0 + 1, step);
+            }
+        }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+#ifdef SEQCDC_TIMELINE
+    if (lane == 0) atomicAdd(&g_lw_stats[0], (unsigned long long)step);
+#endif
+    if (w.single) {
+        // the last warp to finish continues any extension on the valid path that
+        // ran out of budget, with the warp walker on its own (now idle) slots
+        __syncwarp();
+        uint32_t last = 0;
+        if (lane == 0) {
+            __threadfence();
+            last = atomicAdd(w.ctrl + C_DONE, 1u) == gridDim.x * WARPS - 1;
+        }
+        if (__shfl_sync(FULL, last, 0)) {
+            __threadfence();
+            if (*(volatile uint32_t *)(w.ctrl + C_OVF)) {
+                Walker wk;
+                walker_init(wk, sm + (threadIdx.x >> 5) * 32 * STRIDE, w.p, lane);
+                fix_overflows<MODE, M4 ? 4 : 0>(w, wk, lane);
+                walker_finish(wk);
+            }
+        }
+    }
+}
+
+}  // namespace seqcdc
