@@ -44,7 +44,7 @@ def run(args, w: Workload) -> int:
         end = n if rank == world - 1 else min(n, hi + (CudaRangeBackend.TAIL + 1) * p.max_size)
         buf = torch.empty(end - lo, dtype=torch.uint8, device=dev)
         synth.fill_device(w.kind, w.seed, lo, buf)
-        shard = Shard(buf, hi - lo, lo)
+        shard = Shard(buf, hi - lo, lo, n)
         be = CudaRangeBackend(p, device=dev)
         exchange = os.environ.get("SEQCDC_EXCHANGE", "p2p")
         if exchange == "p2p" and not be.enable_p2p():

@@ -221,6 +221,27 @@ def _require_cuda(t, name):
         raise SeqCDCError(f"{name} must be contiguous")
 
 
+def _require_out(t, name, min_numel: int, like, dtype=None):
+    """An output/input tensor the device writes or reads by count: CUDA,
+    contiguous, on `like`'s device, of `dtype` (int64 by default) and with at
+    least `min_numel` elements -- the C ABI takes no capacities, so an
+    undersized tensor is refused here instead of being overrun on the device."""
+    import torch
+    _require_cuda(t, name)
+    if t.device != like.device:
+        raise SeqCDCError(f"{name} is on {t.device}, the data on {like.device}")
+    if t.dtype != (dtype or torch.int64):
+        raise SeqCDCError(f"{name} must be {dtype or torch.int64}, got {t.dtype}")
+    if t.numel() < min_numel:
+        raise SeqCDCError(f"{name} holds {t.numel()} elements, needs >= {min_numel}")
+
+
+def _on(t):
+    """Run a library call with t's device current (kernels, pool and stream agree)."""
+    import torch
+    return torch.cuda.device(t.device)
+
+
 def chunk_into(data, p: SeqParams, cuts, ncuts, workspace=None, stream=None) -> None:
     """Asynchronous: enqueue seqcdc_chunk on ``stream``.  ``data`` uint8 CUDA,
     ``cuts`` int64 CUDA with >= max_cuts(n) entries, ``ncuts`` int64 CUDA [1]."""
@@ -229,11 +250,16 @@ def chunk_into(data, p: SeqParams, cuts, ncuts, workspace=None, stream=None) -> 
     if data.dtype != torch.uint8:
         raise SeqCDCError("data must be uint8")
     n = data.numel()
+    _require_out(cuts, "cuts", max_cuts(n, p), data)
+    _require_out(ncuts, "ncuts", 1, data)
+    if workspace is not None:
+        _require_out(workspace, "workspace", 0, data, torch.uint8)
     cp = p.c()
     ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
-    rc = lib().seqcdc_chunk(data.data_ptr() if n else None, n, ctypes.byref(cp),
-                            cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(), ws_ptr, ws_len,
-                            _stream_ptr(stream, data.device))
+    with _on(data):
+        rc = lib().seqcdc_chunk(data.data_ptr() if n else None, n, ctypes.byref(cp),
+                                cuts.data_ptr() if cuts.numel() else None, ncuts.data_ptr(), ws_ptr, ws_len,
+                                _stream_ptr(stream, data.device))
     _check(rc, "seqcdc_chunk")
 
 
@@ -258,12 +284,17 @@ def chunk_batch_into(data, offsets, p: SeqParams, cuts, cut_index, ncuts, total=
     ns = offsets.numel() - 1
     if total is None:
         total = int(offsets[-1].item() - offsets[0].item())
+    _require_out(offsets, "offsets", 1, data)
+    _require_out(cuts, "cuts", max_cuts_batch(total, ns, p), data)
+    _require_out(cut_index, "cut_index", ns + 1, data)
+    _require_out(ncuts, "ncuts", 1, data)
     cp = p.c()
     ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
-    rc = lib().seqcdc_chunk_batch(data.data_ptr() if data.numel() else None, offsets.data_ptr(), ns, total,
-                                  ctypes.byref(cp), cuts.data_ptr() if cuts.numel() else None,
-                                  cut_index.data_ptr(), ncuts.data_ptr(), ws_ptr, ws_len,
-                                  _stream_ptr(stream, data.device))
+    with _on(data):
+        rc = lib().seqcdc_chunk_batch(data.data_ptr() if data.numel() else None, offsets.data_ptr(), ns, total,
+                                      ctypes.byref(cp), cuts.data_ptr() if cuts.numel() else None,
+                                      cut_index.data_ptr(), ncuts.data_ptr(), ws_ptr, ws_len,
+                                      _stream_ptr(stream, data.device))
     _check(rc, "seqcdc_chunk_batch")
 
 
@@ -296,11 +327,14 @@ def range_chunk_into(buf, range_len: int, entry: int, global_offset: int, p: Seq
     _require_cuda(buf, "buf")
     if buf.dtype != torch.uint8:
         raise SeqCDCError("buf must be uint8")
+    _require_out(cuts, "cuts", range_max_cuts(buf.numel(), range_len, p), buf)
+    _require_out(ncuts, "ncuts", 1, buf)
     cp = p.c()
     ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
-    rc = lib().seqcdc_range_chunk(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len, entry,
-                                  global_offset, ctypes.byref(cp), cuts.data_ptr() if cuts.numel() else None,
-                                  ncuts.data_ptr(), ws_ptr, ws_len, _stream_ptr(stream, buf.device))
+    with _on(buf):
+        rc = lib().seqcdc_range_chunk(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len, entry,
+                                      global_offset, ctypes.byref(cp), cuts.data_ptr() if cuts.numel() else None,
+                                      ncuts.data_ptr(), ws_ptr, ws_len, _stream_ptr(stream, buf.device))
     _check(rc, "seqcdc_range_chunk")
 
 
@@ -310,6 +344,8 @@ def range_resync_into(buf, range_len: int, entry: int, global_offset: int, p: Se
     re-using the speculative chain ``spec[:spec_n]`` after the first common cut.
     ``status`` int64 CUDA [4] = merged, re-walked cuts, merge index, overhang."""
     _require_cuda(buf, "buf")
+    _require_out(cuts, "cuts", range_max_cuts(buf.numel(), range_len, p), buf)
+    _require_out(status, "status", 4, buf)
     cp = p.c()
     rc = lib().seqcdc_range_resync(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len, entry,
                                    global_offset, ctypes.byref(cp), spec.data_ptr() if spec.numel() else None,
@@ -352,6 +388,8 @@ def range_resync_dev_into(buf, range_len: int, d_entry, global_offset: int, p: S
     """Asynchronous seqcdc_range_resync_dev: the entry (a global offset) is read on
     the device from ``d_entry`` (an int64 CUDA tensor element), no host sync."""
     _require_cuda(buf, "buf")
+    _require_out(cuts, "cuts", range_max_cuts(buf.numel(), range_len, p), buf)
+    _require_out(status, "status", 4, buf)
     cp = p.c()
     rc = lib().seqcdc_range_resync_dev(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len,
                                        d_entry.data_ptr(), global_offset, ctypes.byref(cp),
@@ -367,6 +405,9 @@ def range_chunk_tail_into(buf, range_len: int, global_offset: int, p: SeqParams,
     range, and its exchange block (int64 CUDA [3 + tail_max] = overhang, count,
     tail_n, tail)."""
     _require_cuda(buf, "buf")
+    _require_out(cuts, "cuts", range_max_cuts(buf.numel(), range_len, p), buf)
+    _require_out(ncuts, "ncuts", 1, buf)
+    _require_out(block, "block", 3 + tail_max, buf)
     cp = p.c()
     ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
     b0 = block.data_ptr()
@@ -384,6 +425,10 @@ def range_merge_tail_into(buf, range_len: int, global_offset: int, p: SeqParams,
     exchange block; ``sum3`` (optional int64 CUDA [3]) = final overhang, count,
     ``spec_ov[0]``."""
     _require_cuda(buf, "buf")
+    _require_out(prev_block, "prev_block", 3 + tail_max, buf)
+    _require_out(cuts, "cuts", range_max_cuts(buf.numel(), range_len, p), buf)
+    _require_out(ncuts, "ncuts", 1, buf)
+    _require_out(status, "status", 4, buf)
     cp = p.c()
     rc = lib().seqcdc_range_merge_tail(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len,
                                        global_offset, ctypes.byref(cp), prev_block.data_ptr(), tail_max,
@@ -431,6 +476,9 @@ def range_chunk_tail_push_into(buf, range_len: int, global_offset: int, p: SeqPa
     into a mapped peer mailbox (``peer_blk``, 3 + tail_max int64) and releases
     ``flag_value`` to ``peer_flag`` (device addresses from xchg_open)."""
     _require_cuda(buf, "buf")
+    _require_out(cuts, "cuts", range_max_cuts(buf.numel(), range_len, p), buf)
+    _require_out(ncuts, "ncuts", 1, buf)
+    _require_out(block, "block", 3 + tail_max, buf)
     cp = p.c()
     ws_ptr, ws_len = (workspace.data_ptr(), workspace.numel()) if workspace is not None else (None, 0)
     b0 = block.data_ptr()
@@ -450,6 +498,9 @@ def range_merge_tail_wait_into(buf, range_len: int, global_offset: int, p: SeqPa
     mailbox (device address) once ``flag`` reaches ``flag_value`` (waited for on
     the device; a timeout reports overhang UINT64_MAX in ``sum3``)."""
     _require_cuda(buf, "buf")
+    _require_out(cuts, "cuts", range_max_cuts(buf.numel(), range_len, p), buf)
+    _require_out(ncuts, "ncuts", 1, buf)
+    _require_out(status, "status", 4, buf)
     cp = p.c()
     rc = lib().seqcdc_range_merge_tail_wait(buf.data_ptr() if buf.numel() else None, buf.numel(), range_len,
                                             global_offset, ctypes.byref(cp), mailbox, tail_max,

@@ -3,27 +3,28 @@
 // Pipeline for one call (all on the caller's stream, no host synchronisation):
 //   0. reset       one cudaMemsetAsync of the control words + publication
 //                  counters (single stream), or k_setup (batch): the segment
-//                  table -- each stream cut into segments of G bytes, G a
-//                  multiple of max_size.
-//   1. k_walk      persistent CTAs, one warp each.  A CTA takes segments in
-//                  order and walks a SPECULATIVE chain from the segment start
-//                  as if a cut were there ("the next cut depends only on the
-//                  previous cut"), recording cuts < segment end in its list L_s
-//                  (published every 32 cuts with release semantics).  At the
-//                  first cut >= segment end the chain continues (EXTENSION),
-//                  each cut checked against the list of the chain that owns
-//                  that region; the first common cut is a merge point: from
-//                  there on both chains are identical.  Extension cuts go to X_s.
-//   2. k_stitch    per stream (one CTA): follow the merges from the stream start
-//                  (the only chain that is right from its start) to mark live
-//                  chains and where each becomes valid; count valid cuts.  A
-//                  stream whose extension overflowed its budget (pathological
-//                  phase-locked data) is re-walked here by one warp, end to end.
-//                  For a single stream the same CTA also scans the counts.
-//   3. k_scan      (batches only) exclusive scan of per-segment counts.
-//   4. k_copy      gather valid L/X cuts into d_cuts.
-// The hot loop (k_walk) streams every byte HBM->SMEM once with 1-D TMA and
-// classifies lazily; see seqcdc_device.cuh.
+//                  table -- each stream cut into segments of G bytes (G a
+//                  multiple of max_size, except the shortened last segment of a
+//                  range call with a tail).
+//   1. the walk    speculative chains, one per segment, each started at its
+//                  segment start as if a cut were there ("the next cut depends
+//                  only on the previous cut"), recording cuts < segment end in
+//                  L_s and publishing them with release semantics; at the first
+//                  cut >= segment end the chain continues (EXTENSION), each cut
+//                  checked against the list of the chain owning that region; the
+//                  first common cut is a merge point (from there on both chains
+//                  are identical).  Extension cuts go to X_s.
+//                  k_walk  (default): persistent one-warp CTAs, each warp one
+//                          chain; bytes stream HBM->SMEM through a cp.async
+//                          (LDGSTS) ring and are classified lazily, one 128-pair
+//                          window per round (seqcdc_device.cuh).
+//                  k_lwalk (SEQCDC_WALKER=lane): one chain per LANE with sparse
+//                          128-B line fills (seqcdc_lane.cuh).
+//   2. post        single stream, k_walk: one k_post launch (every CTA follows
+//                  the merges and scans the counts itself, then copies its share);
+//                  k_lwalk: k_lpost (valid path over the jumper segments, counts,
+//                  scan) + k_lcopy; batches: k_stitch (per stream: follow merges,
+//                  continue overflowed extensions), k_scan, k_copy.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -55,7 +56,7 @@ constexpr uint64_t G_FLOOR_CHUNKS = 32;   // minimum segment length, in max_size
 constexpr uint64_t G_CEIL = 64ull << 20;  // keeps a chain's span (G + K_EXT*G + max) far below REL_CLAMP
 constexpr uint32_t STITCH_MAX_SEGS = 8000;
 
-enum { C_NSEG = 0, C_NEXT = 1, C_BAD = 3, C_DONE = 4, C_OVF = 5, C_NWORDS = 8 };
+enum { C_NSEG = 0, C_NEXT = 1, C_BAD = 3, C_DONE = 4, C_OVF = 5, C_HAND = 6, C_HNEXT = 7, C_FIN = 8, C_NWORDS = 16 };
 
 struct Work {
     // inputs
@@ -100,6 +101,10 @@ struct Work {
     // into the next range's mailbox (peer memory), then release push_value to *push_flag
     uint64_t *push_blk, *push_flag;
     uint64_t push_value;
+    // lane walker: extensions longer than lw_ext_cap cuts (and a range call's
+    // tail) are handed to warps (task list, zeroed with the control words)
+    uint32_t *hand;
+    uint32_t lw_ext_cap;
 };
 
 struct Seg {
@@ -383,10 +388,12 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
 #pragma unroll 1
     while (base < end_rel) {
         c = resolve<MODE, MSPEC, BR>(wk, w.p, base, lane);
+        SEQCDC_ASSERT_CUT(base, c, w.p, end_rel);
         if (c >= hi_rel) {
             extend = true;
             break;
         }
+        SEQCDC_ASSERT(lb.n < g.Lcap);
         lb_push(lb, off + c, Ls, lane);
         if ((lb.n & 31) == 0) publish(w.Lcnt + s, lb.n, false, lane);
         if (c >= stop_rel) break;
@@ -404,6 +411,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
 #pragma unroll 1
                 while (tb.n < w.tail_max && base + w.p.mx <= end_rel) {
                     c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+                    SEQCDC_ASSERT_CUT(base, c, w.p, end_rel);
                     lb_push(tb, off + c + w.out_add, w.tail, lane);
                     base = c;
                 }
@@ -461,6 +469,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
         }
         base = c;
         c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+        SEQCDC_ASSERT_CUT(base, c, w.p, end_rel);
     }
     lb_flush(xb, Xs, lane);
     TL_MARK(s, 2);
@@ -511,6 +520,7 @@ __device__ uint32_t continue_chain(const Work &w, Walker &wk, const Seg &g, uint
 #pragma unroll 1
         while (base < wk.end_rel && base < stop_at) {
             const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+            SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
             const uint64_t cut = off + c;
             lb_push(lb, cut, dst, lane);
             base = c;
@@ -858,6 +868,7 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
         const uint32_t i = tid + 1024u * u;
         if (i < k) {
             const int64_t e = en[i];
+            SEQCDC_ASSERT(e == ENTRY_DEAD || (uint64_t)(e + 1) <= (uint64_t)lcv[u]);
             cnt[i] = e == ENTRY_DEAD ? 0 : (uint64_t)lcv[u] - (uint64_t)(e + 1) + xcv[u];
         }
     }
@@ -1060,6 +1071,7 @@ __global__ void __launch_bounds__(1024) k_lpost(Work w)
         int64_t e = ENTRY_DEAD;
         if (!(f & 1u)) {
             e = i == 0 ? -1 : ((f & 2u) ? w.entry[i] : __ldcg(w.midx + i - 1));
+            SEQCDC_ASSERT((uint64_t)(e + 1) <= (__ldcg(w.Lcnt + i) & CNT_MASK));
             c = (__ldcg(w.Lcnt + i) & CNT_MASK) - (uint64_t)(e + 1) + __ldcg(w.Xcnt + i) + __ldcg(w.cont_cnt + i);
         }
         w.entry[i] = e;
@@ -1174,6 +1186,17 @@ __global__ void k_push_empty(uint64_t *blk, uint64_t *flag, uint64_t ov, uint64_
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
 }
 
+#ifdef SEQCDC_DEBUG
+// debug builds: the finished cut list is strictly increasing and positive
+__global__ void k_debug_sorted(const uint64_t *cuts, const uint64_t *ncuts)
+{
+    const uint64_t k = *ncuts;
+    if (k == SEQCDC_NCUTS_BAD_INPUT) return;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += (uint64_t)gridDim.x * blockDim.x)
+        SEQCDC_ASSERT(cuts[i] > 0 && (i == 0 || cuts[i] > cuts[i - 1]));
+}
+#endif
+
 __global__ void k_set2(uint64_t *p, uint64_t a, uint64_t b)
 {
     p[0] = a;
@@ -1193,7 +1216,7 @@ struct Plan {
     uint32_t nseg1, capL1, capX1;
     size_t bytes;
     size_t o_ctrl, o_Lcnt, o_str_first, o_cont_cnt, o_seg_lo, o_seg_hi, o_seg_stream, o_Loff, o_Xoff,
-        o_Lcap, o_Xcap, o_Xcnt, o_target, o_midx, o_entry, o_seg_count, o_seg_out, o_L, o_X, o_FB;
+        o_Lcap, o_Xcap, o_Xcnt, o_target, o_midx, o_entry, o_seg_count, o_seg_out, o_L, o_X, o_FB, o_hand;
     uint32_t walk_grid;
     bool lane;             // single stream on the lane walker (k_lwalk + k_lpost + k_lcopy)
 };
@@ -1371,6 +1394,8 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     pl.o_ctrl = take(C_NWORDS * 4);
     pl.o_Lcnt = o;  // contiguous with ctrl: one memset resets both
     o = align_up(o + 8 * S, 256);
+    pl.o_hand = o;  // lane walker task list, also reset by that memset
+    o = align_up(o + (pl.lane ? 4 * (S + S / 32 + 8) : 0), 256);
     pl.o_str_first = take(4ull * (ns + 1));
     pl.o_cont_cnt = take(4 * S);
     pl.o_seg_lo = take(single ? 0 : 8 * S);
@@ -1448,11 +1473,14 @@ static void launch_lane(const Work &w, const Plan &pl, int sms, cudaStream_t st,
     prof_mark(pr, 1, st);
     if (w.p.M == 4) k_lwalk<MODE, true><<<pl.walk_grid, lw::THREADS, 0, st>>>(w);
     else k_lwalk<MODE, false><<<pl.walk_grid, lw::THREADS, 0, st>>>(w);
+    // handed-off extensions / tail on warps, then the post; both wait on the
+    // device (griddepcontrol.wait) for their predecessor: launched early
+    const void *hand = w.p.M == 4 ? (const void *)k_lhand<MODE, 4> : (const void *)k_lhand<MODE, 0>;
+    launch_pdl(hand, dim3(std::max(1, sms * 16)), dim3(32), 0, st, pr == nullptr, w);
     prof_mark(pr, 2, st);
-    // k_lpost waits on the device (griddepcontrol.wait) for the walk: launched early
     launch_pdl((const void *)k_lpost, dim3(1), dim3(1024), 4 * LP_JCAP + pl.nseg1, st, pr == nullptr, w);
     k_lcopy<<<std::max(1, sms * 8), 256, 0, st>>>(w);
-    g_launches += 3;
+    g_launches += 4;
 }
 
 template <int MODE, int MSPEC>
@@ -1559,6 +1587,8 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.L = (uint64_t *)(ws + pl.o_L);
     w.X = (uint64_t *)(ws + pl.o_X);
     w.FB = (uint64_t *)(ws + pl.o_FB);
+    w.hand = pl.lane ? (uint32_t *)(ws + pl.o_hand) : nullptr;
+    w.lw_ext_cap = (uint32_t)std::max(1, env_int("SEQCDC_LW_EXT_CAP", 48));
     w.cuts = d_cuts;
     w.cut_index = d_cut_index;
     w.ncuts = d_ncuts;
@@ -1581,7 +1611,9 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     }
     prof_mark(pr, 0, st);
     if (w.single) {
-        if (cudaMemsetAsync(ws + pl.o_ctrl, 0, pl.o_Lcnt - pl.o_ctrl + 8 * pl.nseg1, st) != cudaSuccess)
+        const size_t zb = pl.lane ? pl.o_hand - pl.o_ctrl + 4 * ((size_t)pl.nseg1 + pl.nseg1 / 32 + 8)
+                                  : pl.o_Lcnt - pl.o_ctrl + 8 * pl.nseg1;
+        if (cudaMemsetAsync(ws + pl.o_ctrl, 0, zb, st) != cudaSuccess)
             return SEQCDC_ECUDA;
     } else {
         k_setup<<<1, 1024, 0, st>>>(w);
@@ -1595,6 +1627,9 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     case 2: launch_ms<2>(ms, w, pl, sms, st, pr); break;
     default: launch_ms<3>(ms, w, pl, sms, st, pr); break;
     }
+#ifdef SEQCDC_DEBUG
+    if (w.single && w.cuts) k_debug_sorted<<<sms, 256, 0, st>>>(w.cuts, w.ncuts);
+#endif
     prof_mark(pr, 3, st);
     if (pr) {
         std::lock_guard<std::mutex> lk(g_mu);

@@ -34,6 +34,26 @@
 
 namespace seqcdc {
 
+// Device-side invariant checks (a -DSEQCDC_DEBUG build; compute-sanitizer is
+// not available on the GPU pool): a violated invariant stops the kernel with
+// __trap(), which the next synchronisation reports as a launch failure.
+#ifdef SEQCDC_DEBUG
+#define SEQCDC_ASSERT(cond)      \
+    do {                         \
+        if (!(cond)) __trap();   \
+    } while (0)
+#else
+#define SEQCDC_ASSERT(cond) \
+    do {                    \
+    } while (0)
+#endif
+
+// A chunk [base, cut) of a stream whose data ends at `end` (relative
+// positions): it is not empty, at most max_size long, and at least
+// min_size long unless it is the stream's last chunk (c9).
+#define SEQCDC_ASSERT_CUT(base, cut, p, end) \
+    SEQCDC_ASSERT((cut) > (base) && (cut) - (base) <= (p).mx && ((cut) - (base) >= (p).mn || (cut) == (end)))
+
 // Ring geometry (profiles/r01/sweeps.md): 2 KiB blocks (4 x 16-byte cp.async per
 // lane each), 4 slots, 2 blocks (4 KiB) in flight ahead of the window.
 #ifndef SEQCDC_BLK_SHIFT
@@ -176,7 +196,7 @@ __device__ __forceinline__ void lt_gt_flags(uint32_t x, uint32_t y, uint32_t &lt
 
 #if !SEQCDC_SPARSE
 // ------------------------------------------------------------------ the shared-memory ring
-// Software-pipelined cp.async ring: 1 KiB blocks are issued strictly in order,
+// Software-pipelined cp.async ring: BLK-byte blocks are issued strictly in order,
 // one cp.async group each; the walk keeps exactly AHEAD groups in flight past
 // the block holding the end of its current window, so `cp.async.wait_group
 // AHEAD` (a constant) proves that window resident.  Block b lives in slot
@@ -203,6 +223,7 @@ __device__ __forceinline__ void ring_issue(Walker &wk, uint32_t b, int lane)
     }
 #endif
     if (b0 >= wk.lo_rel && b0 + BLK <= wk.end_rel) {
+        SEQCDC_ASSERT(b0 + BLK <= REL_CLAMP);
         // a whole block: one base address per side, the k*512 steps become
         // immediate offsets of the copies (a block never wraps the ring)
         const uint32_t dst = wk.buf + (b0 & RING_MASK) + 16 * (uint32_t)lane;
@@ -488,6 +509,7 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
                 first = false;
             }
         }
+        SEQCDC_ASSERT(p0 + 4 > wk.lo_rel && p0 <= lim2);
         const uint32_t q = p0 + qoff;
         // MODE bit 0: Decreasing; bit 1: signed reading (flipping bit 7 of every
         // byte maps int8 order onto uint8 order)

@@ -88,36 +88,56 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr)
 }
 
 // ------------------------------------------------------------------ the lane's byte source
-// Two slots of one LINE each.  A slot holds (or is being filled with) one
-// LINE-aligned line of the job, tagged by its line number.  Fills are 16-byte
-// cp.async copies; every loop step the warp commits one cp.async group and
-// waits until at most LAG groups are in flight, so a fill issued in step t is
-// complete from step t + 1 + LAG on (`rdy`): no barrier, no polling, and the
-// warp only blocks if a fill is older than LAG steps and still not landed.
-#ifndef SEQCDC_LW_LAG
-#define SEQCDC_LW_LAG 2
-#endif
-constexpr uint32_t LAG = SEQCDC_LW_LAG;
-
+// Two slots of one LINE each; line l lives in slot l & 1, so the slots hold
+// consecutive lines and a byte's shared address is base + (x mod 2 LINE).  A
+// fill is 16-byte cp.async copies whose completion arrives on the slot's own
+// mbarrier (cp.async.mbarrier.arrive); a lane polls it with a non-blocking
+// test_wait (a per-thread instruction), so a warp step never waits for memory:
+// lanes whose line has not landed simply do not scan in that step.
 struct Src {
     uint64_t rb;         // absolute address of relative position 0 (LINE-aligned)
     uint32_t lo_rel;     // first byte of the job (relative)
     uint32_t end_rel;    // end of the loadable data (relative, clamped)
     uint32_t sb;         // shared address of this lane's region
-    uint32_t tag0, tag1; // line held by each slot (NONE: none)
-    uint32_t rdy0, rdy1; // first step at which the slot's fill is complete
+    uint32_t tag0, tag1; // line held (or being filled) by each slot (NONE: none)
+    uint32_t pend;       // bit k: slot k's fill not yet seen complete
+    uint32_t par;        // bit k: parity slot k's barrier completes next
 };
 
-// Start filling slot k with line `ln` in step `step` (the slot's previous fill is complete).
-__device__ __forceinline__ void fill(Src &s, uint32_t k, uint32_t ln, uint32_t step)
+__device__ __forceinline__ uint32_t mb_of(const Src &s, uint32_t k) { return s.sb + 2 * LINE + 8 * k; }
+
+__device__ __forceinline__ void mb_init(uint32_t mb)
 {
-    const uint32_t dst = s.sb + k * LINE;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+}
+
+__device__ __forceinline__ void mb_inval(uint32_t mb)
+{
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(mb) : "memory");
+}
+
+__device__ __forceinline__ bool mb_test(uint32_t mb, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(mb), "r"(parity) : "memory");
+    return ok != 0;
+}
+
+// Start filling line `ln` into its slot (whose earlier fill is complete).
+__device__ __forceinline__ void fill(Src &s, uint32_t ln)
+{
+    const uint32_t k = ln & 1u;
+    const uint32_t dst = s.sb + k * LINE, mb = mb_of(s, k);
     const uint32_t x0 = ln << LSH;
-    uint32_t r = step + 1 + LAG;
+#ifdef SEQCDC_TIMELINE
+    atomicAdd(&g_lw_stats[2], 1ull);
+#endif
     if (x0 >= s.lo_rel && x0 + LINE <= s.end_rel) {
         const uint64_t src = s.rb + x0;
 #pragma unroll
         for (uint32_t i = 0; i < LINE; i += 16) cp_async16(dst + i, src + i);
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(mb) : "memory");
     } else {
         // a line at the edge of the data: copy the bytes that exist, one by one
 #pragma unroll 1
@@ -125,34 +145,41 @@ __device__ __forceinline__ void fill(Src &s, uint32_t k, uint32_t ln, uint32_t s
             const uint32_t x = x0 + i;
             if (x >= s.lo_rel && x < s.end_rel) sts8(dst + i, *(const volatile uint8_t *)(s.rb + x));
         }
-        r = step;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb) : "memory");
     }
-#ifdef SEQCDC_TIMELINE
-    atomicAdd(&g_lw_stats[2], 1ull);
-#endif
-    if (k) {
-        s.tag1 = ln;
-        s.rdy1 = r;
-    } else {
-        s.tag0 = ln;
-        s.rdy0 = r;
-    }
+    if (k) s.tag1 = ln; else s.tag0 = ln;
+    s.pend |= 1u << k;
 }
 
-// Line l lives in slot l & 1, so the two slots always hold consecutive lines
-// and a byte's shared address is just base + (x mod 2 LINE).
+// Poll the slots with a fill in flight (one non-blocking barrier test each).
+__device__ __forceinline__ void poll(Src &s)
+{
+#pragma unroll
+    for (uint32_t k = 0; k < 2; k++)
+        if (((s.pend >> k) & 1u) && mb_test(mb_of(s, k), (s.par >> k) & 1u)) {
+            s.pend &= ~(1u << k);
+            s.par ^= 1u << k;
+        }
+}
+
+__device__ __forceinline__ void drain(Src &s)
+{
+#pragma unroll 1
+    while (s.pend) poll(s);
+}
+
 __device__ __forceinline__ bool has(const Src &s, uint32_t ln) { return ((ln & 1u) ? s.tag1 : s.tag0) == ln; }
 
-// Is line ln resident and complete in step `step`?
-__device__ __forceinline__ bool ready(const Src &s, uint32_t ln, uint32_t step)
+// Is line ln resident and complete?
+__device__ __forceinline__ bool ready(const Src &s, uint32_t ln)
 {
-    return (ln & 1u) ? (s.tag1 == ln && step >= s.rdy1) : (s.tag0 == ln && step >= s.rdy0);
+    return has(s, ln) && !((s.pend >> (ln & 1u)) & 1u);
 }
 
-// Start filling line ln into its slot unless the slot's earlier fill is still in flight.
-__device__ __forceinline__ void request(Src &s, uint32_t ln, uint32_t step)
+// Start filling line ln unless its slot's earlier fill is still in flight.
+__device__ __forceinline__ void request(Src &s, uint32_t ln)
 {
-    if (step >= ((ln & 1u) ? s.rdy1 : s.rdy0)) fill(s, ln & 1u, ln, step);
+    if (!((s.pend >> (ln & 1u)) & 1u)) fill(s, ln);
 }
 
 __device__ __forceinline__ uint32_t slot_addr(const Src &s, uint32_t x) { return s.sb + (x & (2 * LINE - 1)); }
@@ -266,6 +293,22 @@ __device__ __forceinline__ uint32_t scan_group(Chain &c, const Src &s, const Dev
     return NONE;
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Publish a task for the warps (segment s's extension, or with `tail` the
+// range call's tail): its list writes are ordered before the release store.
+__device__ __forceinline__ void hand_off(const Work &w, uint32_t s, bool tail)
+{
+    const uint32_t idx = atomicAdd(w.ctrl + C_HAND, 1u);
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(w.hand + idx), "r"((s + 1) | (tail ? 0x80000000u : 0u))
+                 : "memory");
+}
+
 // A cut of lane s's chain at relative position `cut`: record it where the
 // phase says (speculative list, extension list with the merge check, or the
 // range tail) and decide whether the chain goes on.  Returns false when the
@@ -299,25 +342,9 @@ __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, 
             c.ph = PH_DONE;
             return false;
         }
-        // range call: the chain continues past the overhang (the next rank's merge)
-        c.ph = PH_TAIL;
-        c.list = w.tail;
-        c.n = 0;
-        bool more = false;
-        if (cut < src.end_rel) {
-            c.list[c.n++] = cabs + w.out_add;
-            more = c.n < w.tail_max && cut + w.p.mx <= src.end_rel;
-        }
-        if (!more) {
-            *w.tail_n = c.n;
-            c.ph = PH_DONE;
-        }
-        return more;
-    }
-    if (c.ph == PH_TAIL) {
-        c.list[c.n++] = cabs + w.out_add;
-        if (c.n < w.tail_max && cut + w.p.mx <= src.end_rel) return true;
-        *w.tail_n = c.n;
+        // range call: the chain continues past the overhang (the next rank's
+        // merge) -- handed to a warp, which walks the ~100 chunks much faster
+        hand_off(w, s, true);
         c.ph = PH_DONE;
         return false;
     }
@@ -358,7 +385,13 @@ __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, 
                     c.j++;
                     c.cand = __ldcg(w.L + c.t_Loff + c.j);
                 }
-                if (c.cand != cabs) return true;        // not a cut of the owning chain: walk on
+                if (c.cand != cabs) {                   // not a cut of the owning chain: walk on
+                    if (c.n < w.lw_ext_cap) return true;
+                    w.Xcnt[s] = c.n;                    // a long extension: a warp continues it
+                    hand_off(w, s, false);
+                    c.ph = PH_DONE;
+                    return false;
+                }
                 tgt = (int32_t)c.t;
                 mi = (int64_t)c.j;
             }
@@ -377,6 +410,94 @@ __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, 
 
 
 }  // namespace lw
+
+// A task handed off by a lane, served by a whole warp with the warp walker
+// (dense cp.async ring in the warp's idle lane slots, seqcdc_device.cuh):
+// continue segment s's extension from its last cut until a cut coincides with
+// the chain owning its region (as walk_segment's extension does), or walk a
+// range call's tail (up to tail_max cuts past the overhang, only chunks wholly
+// inside the buffer).
+template <int MODE, int MSPEC>
+__device__ void lw_serve(const Work &w, Walker &wk, uint32_t task, int lane)
+{
+    const uint32_t s = (task & 0x7fffffffu) - 1;
+    const bool tail = task >> 31;
+    const uint64_t abase = (uint64_t)(uintptr_t)w.in;
+    const Seg g = get_seg(w, s);
+    if (tail) {
+        const uint64_t nl = __ldcg(w.Lcnt + s) & CNT_MASK;
+        const uint64_t from = __ldcg(w.L + g.Loff + nl - 1);          // the overhang
+        uint32_t base = walker_begin(wk, abase + from, abase + g.E);
+        const uint64_t off = wk.rb - abase;
+        ListBuf tb{0, 0};
+        if (base < wk.end_rel) {
+            lb_push(tb, from + w.out_add, w.tail, lane);
+#pragma unroll 1
+            while (tb.n < w.tail_max && base + w.p.mx <= wk.end_rel) {
+                const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+                SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
+                lb_push(tb, off + c + w.out_add, w.tail, lane);
+                base = c;
+            }
+        }
+        lb_flush(tb, w.tail, lane);
+        if (lane == 0) *w.tail_n = tb.n;
+        return;
+    }
+    uint64_t *Xs = w.X + g.Xoff;
+    const uint32_t n0 = __ldcg(w.Xcnt + s);
+    const uint64_t from = __ldcg(Xs + n0 - 1);
+    ListBuf xb;
+    xb.n = n0;
+    xb.v = lane < (int)(n0 & 31) ? __ldcg(Xs + (n0 & ~31u) + lane) : 0;   // the open batch
+    uint32_t base = walker_begin(wk, abase + from, abase + g.E);
+    const uint64_t off = wk.rb - abase;
+    const uint64_t stop_abs = w.single ? w.stop : g.E;
+    const uint64_t ext_end = g.hi + K_EXT * w.G;
+    uint32_t t = g.first + (uint32_t)((from - g.S0) / w.G);
+    uint64_t t_next = seg_start(w, g, t + 1);
+    Cursor cur{-1, 0, 0, 0};
+    uint64_t t_lo = 0, t_Loff = 0;
+    int32_t tgt = TGT_OVERFLOW;
+    int64_t mi = -1;
+#pragma unroll 1
+    for (;;) {
+        const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+        SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
+        const uint64_t cut = off + c;
+        if (xb.n == g.Xcap || cut > ext_end) break;                     // budget exhausted: overflow
+        lb_push(xb, cut, Xs, lane);
+        if (cut >= stop_abs) {
+            tgt = TGT_END;
+            break;
+        }
+#pragma unroll 1
+        while (cut >= t_next) {
+            t++;
+            t_next += w.G;
+        }
+        if ((int64_t)t != cur.t) {
+            t_lo = seg_start(w, g, t);
+            t_Loff = w.single ? (uint64_t)t * w.capL1 : w.Loff[t];
+        }
+        int64_t idx;
+        if (check_cut(w, cur, t, t_lo, t_Loff, cut, idx, lane) == CK_MERGE) {
+            tgt = (int32_t)t;
+            mi = idx;
+            break;
+        }
+        base = c;
+    }
+    lb_flush(xb, Xs, lane);
+    if (lane == 0) {
+        w.Xcnt[s] = xb.n;
+        w.target[s] = tgt;
+        w.midx[s] = mi;
+        w.cont_cnt[s] = 0;
+        if (tgt == TGT_OVERFLOW) atomicOr(w.ctrl + C_OVF, 1u);
+    }
+    __syncwarp();
+}
 
 // The per-lane walker kernel.  One segment per lane (grid = segments / THREADS).
 template <int MODE, bool M4>
@@ -397,8 +518,11 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
         asm volatile("mov.b32 %0, %0;" : "+r"(sb));
         src.sb = sb;
     }
+    mb_init(mb_of(src, 0));
+    mb_init(mb_of(src, 1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     src.tag0 = src.tag1 = NONE;
-    src.rdy0 = src.rdy1 = 0;
+    src.pend = src.par = 0;
 
     Chain c;
     c.ph = PH_DONE;
@@ -438,17 +562,16 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
     uint32_t step = 0;
 #pragma unroll 1
     while (__any_sync(FULL, c.ph != PH_DONE)) {
-        cp_async_commit();
-        cp_async_wait<LAG>();
         step++;
         if (c.ph == PH_DONE) continue;
+        if (src.pend) poll(src);
         uint32_t cut = pend;
         pend = NONE;
         if (cut == NONE) {
             const uint32_t l0 = c.q >> LSH;
             // byte q+16 lies in the next line only for the line's last group
             const bool two = (c.q & LMASK) == LINE - 16 && c.q + 16 <= c.lim2 + 1;
-            if (ready(src, l0, step) && (!two || ready(src, l0 + 1, step))) {
+            if (ready(src, l0) && (!two || ready(src, l0 + 1))) {
                 cut = scan_group<MODE, M4>(c, src, p);
 #ifdef SEQCDC_TIMELINE
                 atomicAdd(&g_lw_stats[1], 1ull);
@@ -456,7 +579,9 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
             }
         }
         if (cut != NONE) {
+            SEQCDC_ASSERT_CUT(c.base, cut, p, src.end_rel);
             if (c.ph == PH_SPEC && cut < c.hi_rel && cut < c.stop_rel) {   // the common case
+                SEQCDC_ASSERT(c.n < c.cap);
                 c.list[c.n++] = c.off + cut;
                 if (!chunk_begin(c, src, p, cut)) pend = c.limit;
             } else if (on_cut(w, c, src, g, s, stop_abs, cut)) {
@@ -466,36 +591,56 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
         if (c.ph != PH_DONE && pend == NONE) {          // the lines the next groups need, on their way
             const uint32_t l0 = c.q >> LSH;
             if (!has(src, l0)) {
-                request(src, l0, step);
+                request(src, l0);
             } else if ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) && ((l0 + 1) << LSH) < src.end_rel) {
-                request(src, l0 + 1, step);
+                request(src, l0 + 1);
             }
         }
     }
-    cp_async_wait<0>();
+    drain(src);
+    mb_inval(mb_of(src, 0));
+    mb_inval(mb_of(src, 1));
     __syncwarp();
 #ifdef SEQCDC_TIMELINE
     if (lane == 0) atomicAdd(&g_lw_stats[0], (unsigned long long)step);
 #endif
+}
+
+// The handed-off tasks, after the lane walk (stream order): persistent
+// one-warp CTAs claim tasks until none is left; then the last warp to finish
+// continues any extension on the valid path that ran out of budget (single
+// stream; as k_walk does).
+template <int MODE, int MSPEC>
+__global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_lhand(Work w)
+{
+    __shared__ __align__(128) uint8_t ring[RING];
+    asm volatile("griddepcontrol.wait;" ::: "memory");      // the lane walk complete
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int lane = threadIdx.x;
+    Walker wk;
+    walker_init(wk, ring, w.p, lane);
+    const uint32_t ntask = *(volatile uint32_t *)(w.ctrl + C_HAND);
+#pragma unroll 1
+    for (;;) {
+        uint32_t j = 0;
+        if (lane == 0) j = atomicAdd(w.ctrl + C_HNEXT, 1u);
+        j = __shfl_sync(FULL, j, 0);
+        if (j >= ntask) break;
+        lw_serve<MODE, MSPEC>(w, wk, __ldcg(w.hand + j), lane);
+    }
     if (w.single) {
-        // the last warp to finish continues any extension on the valid path that
-        // ran out of budget, with the warp walker on its own (now idle) slots
         __syncwarp();
         uint32_t last = 0;
         if (lane == 0) {
             __threadfence();
-            last = atomicAdd(w.ctrl + C_DONE, 1u) == gridDim.x * WARPS - 1;
+            last = atomicAdd(w.ctrl + C_DONE, 1u) == gridDim.x - 1;
         }
         if (__shfl_sync(FULL, last, 0)) {
             __threadfence();
-            if (*(volatile uint32_t *)(w.ctrl + C_OVF)) {
-                Walker wk;
-                walker_init(wk, sm + (threadIdx.x >> 5) * 32 * STRIDE, w.p, lane);
-                fix_overflows<MODE, M4 ? 4 : 0>(w, wk, lane);
-                walker_finish(wk);
-            }
+            if (*(volatile uint32_t *)(w.ctrl + C_OVF)) fix_overflows<MODE, MSPEC>(w, wk, lane);
         }
     }
+    walker_finish(wk);
 }
 
 }  // namespace seqcdc

@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(128) k_merge_tail(const uint64_t *blk, uint32_
                                                     uint64_t timeout_ns)
 {
     __shared__ unsigned long long best;                  // (i << 32) | j of the first merge
+    __shared__ unsigned long long tcap_s;                // first tail entry at or past the range end
     __shared__ int timed_out;
     if (wait_flag) {
         if (threadIdx.x == 0) {
@@ -226,7 +227,16 @@ __global__ void __launch_bounds__(128) k_merge_tail(const uint64_t *blk, uint32_
         }
         return;
     }
-    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    // the true chain's first cut at or past this range's end caps the search: a
+    // merge found only beyond it would hand this range cuts of the next one, so
+    // then the re-walk decides (and reports the changed overhang)
+    if (threadIdx.x == 0) tcap_s = ~0ull;
+    __syncthreads();
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x)
+        if (__ldcg(e + i) >= a.gofs + a.stop) atomicMin(&tcap_s, (unsigned long long)i);
+    __syncthreads();
+    const uint64_t lim = min(n, (uint64_t)tcap_s + 1);
+    for (uint64_t i = threadIdx.x; i < lim; i += blockDim.x) {
         const uint64_t x = __ldcg(e + i);
         uint64_t lo = 0, hi = k;                         // binary search in the ascending spec list
         while (lo < hi) {

@@ -46,11 +46,13 @@ class Shard:
     """Rank-local piece of a stream: ``buf`` = bytes [global_offset,
     global_offset + len(buf)): the range (first ``range_len`` bytes) plus a
     right halo of >= max_size - 1 bytes, or, for the last rank, exactly the
-    rest of the stream."""
+    rest of the stream.  ``stream_len`` (optional) lets a non-final range's
+    halo be shorter when it reaches the end of the stream."""
 
     buf: Any
     range_len: int
     global_offset: int
+    stream_len: int | None = None
 
 
 @dataclass
@@ -103,8 +105,16 @@ def chunk_sharded(shard: Shard, backend, group=None, comm_device=None) -> ShardR
     P = dist.get_world_size(group)
     r = dist.get_rank(group)
     dev = comm_device if comm_device is not None else backend.comm_device
-    if P > 1 and r < P - 1 and shard.range_len < backend.max_size:
-        raise ValueError("a non-final range must hold at least max_size bytes")
+    if P > 1 and r < P - 1:
+        if shard.range_len < backend.max_size:
+            raise ValueError("a non-final range must hold at least max_size bytes")
+        # the chunk starting at the range's last true cut (< range end) reads up to
+        # max_size - 1 bytes past the range end: without that right halo the
+        # range call would treat the buffer end as the stream end and force a cut there
+        at_end = shard.stream_len is not None and shard.global_offset + len(shard.buf) >= shard.stream_len
+        if len(shard.buf) < shard.range_len + backend.max_size - 1 and not at_end:
+            raise ValueError("a non-final range needs a right halo of >= max_size - 1 bytes "
+                             f"(buffer {len(shard.buf)} < range {shard.range_len} + {backend.max_size - 1})")
     if getattr(backend, "device_protocol", False) and getattr(dev, "type", str(dev)) != "cpu":
         done = _device_round(shard, backend, group, P, r)
         if done is not None:

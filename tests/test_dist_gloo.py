@@ -60,7 +60,7 @@ def _worker(rank, P, port, case, uneven, q):
         R = _bounds(n, P, p.max_size, uneven)
         lo, hi = R[rank], R[rank + 1]
         end = n if rank == P - 1 else min(n, hi + p.max_size)
-        shard = Shard(b[lo:end], hi - lo, lo)
+        shard = Shard(b[lo:end], hi - lo, lo, n)
         res = chunk_sharded(shard, OracleRangeBackend(p))
         cuts = [int(c) for c in np.asarray(res.cuts)[: res.count]]
         allc = [None] * P
@@ -71,7 +71,8 @@ def _worker(rank, P, port, case, uneven, q):
         dist.destroy_process_group()
 
 
-RUNS = [(2, c) for c in CASES] + [(3, "markov4k_dec"), (3, "zeros"), (3, "dec_ramp"), (4, "uniform8k"), (4, "zeros")]
+RUNS = [(2, c) for c in CASES] + [(3, "markov4k_dec"), (3, "zeros"), (3, "dec_ramp"), (4, "uniform8k"), (4, "zeros"),
+                                   (8, "uniform8k"), (8, "zeros"), (8, "dec_ramp")]
 
 
 @pytest.mark.parametrize("P,case", RUNS)
@@ -100,6 +101,43 @@ def test_sharded_equals_single_stream(P, case):
     assert np.array_equal(np.asarray(got, np.uint64), want), case
     if case == "zeros" and P >= 3:
         assert max(r[3] for r in allc) >= 2      # overhang changes cascaded (several rounds)
+
+
+def _halo_worker(rank, P, port, halo, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        from paper_2505_21194_b200.dist import Shard, chunk_sharded
+        from tests.oracle_range import OracleRangeBackend
+        p = oracle.table1(8)
+        b = synth.fill_host("uniform", 31, 0, 1 << 20)
+        lo, hi = (0, 1 << 19) if rank == 0 else (1 << 19, 1 << 20)
+        end = min(b.size, hi + halo) if rank == 0 else b.size
+        err = ""
+        if rank == 0:                  # the check runs before any collective
+            try:
+                chunk_sharded(Shard(b[lo:end], hi - lo, lo), OracleRangeBackend(p))
+            except ValueError as e:
+                err = str(e)
+        q.put((rank, err))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("halo,raises", [(0, True), (16382, True)])
+def test_non_final_range_needs_a_right_halo(halo, raises):
+    """A non-final range without max_size - 1 bytes past its end would take the
+    buffer end for the stream end and force a cut there: refused."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, 2, port, halo, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=240) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+    assert bool(res[0]) == raises, res
 
 
 def test_lpt_assign_balances_and_partitions():

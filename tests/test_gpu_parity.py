@@ -60,6 +60,15 @@ def _reset_segments():
     sc.set_segment_bytes(0)
 
 
+@pytest.fixture(params=["warp", "lane"])
+def walker(request, monkeypatch):
+    """Run a single-stream test on both walkers: the warp-cooperative dense one
+    and the per-lane sparse one (seqcdc_lane.cuh; it takes M <= 4 runs only,
+    other parameter sets stay on the warp walker)."""
+    monkeypatch.setenv("SEQCDC_WALKER", request.param)
+    return request.param
+
+
 # ------------------------------------------------------------------ exhaustive tiny inputs
 GRID = [(2, 2, 2, 1, 0), (2, 2, 3, 1, 1), (2, 3, 5, 2, 0), (3, 3, 4, 2, 0), (3, 4, 7, 1, 3),
         (3, 5, 8, 3, 1), (4, 4, 8, 2, 1)]
@@ -122,7 +131,7 @@ KIND_CASES = [
 
 
 @pytest.mark.parametrize("kind,seed,n,p", KIND_CASES)
-def test_single_stream_kinds(kind, seed, n, p):
+def test_single_stream_kinds(kind, seed, n, p, walker):
     b = synth.fill_host(kind, seed, 0, n)
     want = oracle.chunk(b, p)
     _assert_same(_gpu_chunk(b, p), want, kind)
@@ -132,7 +141,7 @@ def test_single_stream_kinds(kind, seed, n, p):
 @pytest.mark.parametrize("kind,p", [("uniform", oracle.table1(8)), ("markov", oracle.table1(4, 1)),
                                     ("rampmix", oracle.table1(8)), ("zeroheavy", oracle.table1(16)),
                                     ("uniform", oracle.table1(16))])
-def test_segment_size_independence(G, kind, p):
+def test_segment_size_independence(G, kind, p, walker):
     """Cut lists do not depend on the speculative segment length (many seams,
     extensions spanning several segments)."""
     b = synth.fill_host(kind, 11, 0, 12 << 20)
@@ -143,7 +152,7 @@ def test_segment_size_independence(G, kind, p):
 
 @pytest.mark.parametrize("name", ["zeros", "const7", "inc_ramp", "dec_ramp", "alt2", "sawtooth"])
 @pytest.mark.parametrize("G", [0, 1 << 16])
-def test_phase_locked_and_degenerate(name, G):
+def test_phase_locked_and_degenerate(name, G, walker):
     n = 6 << 20
     i = np.arange(n)
     b = {"zeros": np.zeros(n), "const7": np.full(n, 7), "inc_ramp": i % 256, "dec_ramp": (255 - i) % 256,
@@ -154,13 +163,13 @@ def test_phase_locked_and_degenerate(name, G):
 
 
 @pytest.mark.parametrize("offset", list(range(1, 16)))
-def test_unaligned_input(offset):
+def test_unaligned_input(offset, walker):
     b = synth.fill_host("rampmix", 100 + offset, 0, (1 << 20) + offset * 7)
     p = oracle.table1(8)
     _assert_same(_gpu_chunk(b, p, offset=offset), oracle.chunk(b, p), f"offset {offset}")
 
 
-def test_edge_sizes():
+def test_edge_sizes(walker):
     p = oracle.Params(0, 5, 50, 256, 4096, 16384)
     L, mn, mx = p.seq_length, p.min_size, p.max_size
     for n in [0, 1, 2, L - 1, L, L + 1, mn - 1, mn, mn + 1, mx - 1, mx, mx + 1, 2 * mx + 3, 3 * TILE_HINT + 5]:
@@ -171,7 +180,7 @@ def test_edge_sizes():
 TILE_HINT = 2048
 
 
-def test_parameter_extremes():
+def test_parameter_extremes(walker):
     rng = np.random.default_rng(5)
     b = _random_stream(rng, 300_000)
     for p in [oracle.Params(0, 2, 1, 0, 2, 2), oracle.Params(1, 16, 1, 1000, 16, 16),

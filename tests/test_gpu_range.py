@@ -114,8 +114,8 @@ def _worker(rank, P, port, kind, seed, n, pidx, q, comm="cpu"):
             be.enable_p2p()
             comm = "cuda"
         cd = torch.device(comm)
-        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=cd)
-        res = chunk_sharded(Shard(buf, hi - lo, lo), be, comm_device=cd)   # buffers (and mailboxes) reused
+        res = chunk_sharded(Shard(buf, hi - lo, lo, n), be, comm_device=cd)
+        res = chunk_sharded(Shard(buf, hi - lo, lo, n), be, comm_device=cd)   # buffers (and mailboxes) reused
         path = be.last_path
         cuts = res.cuts[: res.count].cpu().numpy().tolist()
         allc = [None] * P
