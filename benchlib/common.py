@@ -47,7 +47,10 @@ CFG2 = Workload("cfg2", "config 2: 1 GiB order-1 Markov text (seed 2); Decreasin
                 "SkipSize 256, min 2 KiB, max 8 KiB", "markov", 2, GiB, 4, 1)
 RAMP4G = Workload("rampmix4g", "north-star line: 4 GiB + 12345 B of the config-5 generator; Increasing, L5 T50 S256, "
                   "min 4 KiB, max 16 KiB", "rampmix", 5, 4 * GiB + 12345, 8, 0)
-WORKLOADS = {w.key: w for w in (CFG5, CFG2, RAMP4G)}
+CFG4 = Workload("cfg4", "config 4: versioned backup stream, 4 GiB uniform base + 10 versions with seeded 1% edits "
+                "(inserts/deletes/overwrites of 1 B-4 KiB), ~44 GiB, one stream; Increasing, SeqLength 5, SkipTrigger 50, "
+                "SkipSize 512, min 8 KiB, max 32 KiB", "versions", 4, 47240893232, 16, 0)
+WORKLOADS = {w.key: w for w in (CFG5, CFG2, RAMP4G, CFG4)}
 
 
 def peaks():
@@ -61,13 +64,26 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def traffic(kernel: str, workload_key: str, lib_tag: str):
+def src_hash() -> str:
+    """Hash of the library's sources (csrc/ + include/): identifies the build an
+    ncu capture was taken with."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in (os.path.join(ROOT, "paper_2505_21194_b200", "csrc"), os.path.join(ROOT, "include")):
+        for f in sorted(os.listdir(d)):
+            if f.endswith((".cu", ".cuh", ".h")):
+                with open(os.path.join(d, f), "rb") as fh:
+                    h.update(f.encode() + fh.read())
+    return h.hexdigest()[:16]
+
+
+def traffic(kernel: str, workload_key: str):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
-    (profiles/traffic.json), if it was taken on this workload with this build."""
+    (profiles/traffic.json), if it was taken on this workload with these sources."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             d = json.load(f)[f"{kernel}:{workload_key}"]
-        if d.get("lib_tag") != lib_tag:
+        if d.get("src_hash") != src_hash():
             return None, None
         return int(d["dram_read_bytes"]) + int(d["dram_write_bytes"]), d.get("source")
     except Exception:

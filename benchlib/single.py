@@ -7,7 +7,7 @@ import time
 import numpy as np
 import torch
 
-from .common import METRIC, ClockSampler, Workload, cpu_desc, peaks, step_stats, traffic
+from .common import METRIC, ClockSampler, Workload, cpu_desc, peaks, src_hash, step_stats, traffic
 
 
 class Stream:
@@ -18,8 +18,12 @@ class Stream:
         import paper_2505_21194_b200 as sc
         self.w, self.dev = w, dev
         self.p = sc.SeqParams.table1(w.avg_kib, w.mode)
-        self.data = torch.empty(w.n, dtype=torch.uint8, device=dev)
-        synth.fill_device(w.kind, w.seed, 0, self.data)
+        if w.kind == "versions":                 # config 4: the versioned stream is built as a piece table
+            self.data, _ = synth.versions_device(w.seed, 4 << 30, device=dev)
+            assert self.data.numel() == w.n, (self.data.numel(), w.n)
+        else:
+            self.data = torch.empty(w.n, dtype=torch.uint8, device=dev)
+            synth.fill_device(w.kind, w.seed, 0, self.data)
         self.cuts = torch.empty(max(sc.max_cuts(w.n, self.p), 1), dtype=torch.int64, device=dev)
         self.ncuts = torch.zeros(1, dtype=torch.int64, device=dev)
         self.ws = torch.empty(sc.workspace_size(w.n, 1, self.p), dtype=torch.uint8, device=dev)
@@ -111,8 +115,25 @@ def e2e(st: Stream, host_in: torch.Tensor, steps: int):
                    "per step (wall clock around synchronised steps)"}
 
 
-def extra_line(w: Workload, dev, steps: int, warmup: int) -> dict:
-    """A secondary workload (not the headline): K timed calls + whole-list parity."""
+def extra_line(w: Workload, dev, steps: int, warmup: int, walker: str | None = None) -> dict:
+    """A secondary workload (not the headline): K timed calls + whole-list parity
+    (`walker` forces SEQCDC_WALKER for this line)."""
+    from . import verify
+    import paper_2505_21194_b200 as sc
+    old = os.environ.get("SEQCDC_WALKER")
+    if walker:
+        os.environ["SEQCDC_WALKER"] = walker
+    try:
+        return _extra_line(w, dev, steps, warmup) | {"walker": walker or "auto", "lib": sc.build_info()}
+    finally:
+        if walker:
+            if old is None:
+                os.environ.pop("SEQCDC_WALKER", None)
+            else:
+                os.environ["SEQCDC_WALKER"] = old
+
+
+def _extra_line(w: Workload, dev, steps: int, warmup: int) -> dict:
     from . import verify
     st = Stream(w, dev)
     ms, per, _ = st.timed(steps, warmup)
@@ -157,10 +178,11 @@ def run(args, w: Workload) -> int:
     walk_ms = phases["walk"]
     alg = chk.get("touched_bytes", {}).get("32B_units")
     achieved = alg / (walk_ms / 1e3) / 1e9 if alg else None
-    tr, tr_src = traffic("k_walk", w.key, lib_tag)
+    kernel = "k_lwalk" if "last call: lane walker" in lib_tag else "k_walk"
+    tr, tr_src = traffic(kernel, w.key)
     roof = {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4) if achieved else None, "traffic": tr,
-            "kernel": "k_walk", "kernel_ms": round(walk_ms, 4), "algorithmic_bytes": alg,
+            "kernel": kernel, "kernel_ms": round(walk_ms, 4), "algorithmic_bytes": alg,
             "algorithmic_def": "32-B sectors (stream-aligned) holding a byte of a pair the method compares, counted "
                                "by the instrumented oracle over the whole stream (SURVEY.md 8(d)); the sub-minimum "
                                "and skipped regions are never read by the method (P:179, P:189)",
@@ -170,13 +192,15 @@ def run(args, w: Workload) -> int:
                            "source": tr_src} if tr else None),
             "touched_fraction": chk.get("touched_fraction"),
             "peak_source": peak_src, "share_of_step": round(walk_ms / phases["call"], 3),
-            "kernel_timing": "CUDA events around k_walk on the launching stream (library profile hooks), "
+            "kernel_timing": f"CUDA events around {kernel} on the launching stream (library profile hooks), "
                              "second region of K steps"}
     extras = {}
     if not args.no_extras:
         from .common import CFG2, RAMP4G
         for ew in (CFG2, RAMP4G):
             extras[ew.key] = extra_line(ew, dev, max(5, min(args.steps, 20)), args.warmup)
+        if kernel == "k_lwalk":          # the same stream on the dense warp walker, for comparison
+            extras[w.key + "_warp_walker"] = extra_line(w, dev, max(5, min(args.steps, 10)), args.warmup, "warp")
     ok = chk["bit_exact"] and all(e["bit_exact"] for e in extras.values())
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
@@ -201,6 +225,7 @@ def run(args, w: Workload) -> int:
         "gpu_launches": launches,
         "gpu_launches_per_step": round(launches / args.steps, 2),
         "lib": lib_tag,
+        "src_hash": src_hash(),
         "also": extras,
     }
     print(json_dumps(line), flush=True)

@@ -967,50 +967,73 @@ __device__ __forceinline__ uint32_t tgt_of(const Work &w, uint32_t i, uint32_t k
     return t >= 0 ? (uint32_t)t : k;               // the stream (range) end
 }
 
-__global__ void __launch_bounds__(1024) k_lpost(Work w)
+// Block-wide exclusive scan of one value per thread (512 threads = 16 warps);
+// returns the exclusive prefix, *tot the block total.
+template <typename T>
+__device__ __forceinline__ T block_excl(T v, T *ws, T &tot)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const T x = lane < nw ? ws[lane] : 0;
+        T xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T t = __shfl_up_sync(FULL, xi, o);
+            if (lane >= o) xi += t;
+        }
+        ws[lane] = xi - x;
+        if (lane == 31) ws[32] = xi;
+    }
+    __syncthreads();
+    const T r = ws[wid] + inc - v;
+    tot = ws[32];
+    __syncthreads();
+    return r;
+}
+
+constexpr uint32_t LP_TILE = 512, LP_BATCH = 8;   // one segment per thread per tile, 8 tiles per load round
+
+__global__ void __launch_bounds__(512) k_lpost(Work w)
 {
     extern __shared__ __align__(128) uint8_t sm[];
     asm volatile("griddepcontrol.wait;" ::: "memory");   // the walk complete and its writes visible
     const uint32_t k = w.nseg1;
     uint32_t *jl = (uint32_t *)sm;                 // [LP_JCAP] jumpers in ascending order
     uint8_t *fl = sm + 4 * LP_JCAP;                // [k]: bit 0 dead, bit 1 entry written by a live jumper
-    __shared__ uint32_t nj_s, wsum32[32];
-    __shared__ uint64_t wsum64[32];
-    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    __shared__ uint32_t ws32[33];
+    __shared__ uint64_t ws64[33];
+    const uint32_t tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
-    const uint32_t per = (k + nt - 1) / nt;
-    const uint32_t b0 = min(k, tid * per), b1 = min(k, b0 + per);
-    // A. flags cleared; jumpers counted per thread, then placed in order
-    uint32_t cj = 0;
-    for (uint32_t i = b0; i < b1; i++) {
-        fl[i] = 0;
-        if (i + 1 < k && tgt_of(w, i, k) != i + 1) cj++;
-    }
-    uint32_t inc = cj;
+    // A. jumpers (target != s + 1), in ascending order: coalesced tiles, order-
+    // preserving compaction per tile
+    uint32_t nj = 0;
+    for (uint32_t base = 0; base < k; base += LP_TILE * LP_BATCH) {
+        int32_t t8[LP_BATCH];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, inc, o);
-        if (lane >= o) inc += t;
-    }
-    if (lane == 31) wsum32[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-        const uint32_t x = lane < (int)(nt >> 5) ? wsum32[lane] : 0;
-        uint32_t xi = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(FULL, xi, o);
-            if (lane >= o) xi += t;
+        for (uint32_t u = 0; u < LP_BATCH; u++) {
+            const uint32_t i = base + u * LP_TILE + tid;
+            t8[u] = i < k ? __ldcg(w.target + i) : 0;
         }
-        wsum32[lane] = xi - x;
-        if (lane == 31) nj_s = xi;
+#pragma unroll
+        for (uint32_t u = 0; u < LP_BATCH; u++) {
+            const uint32_t i = base + u * LP_TILE + tid;
+            const uint32_t t = t8[u] >= 0 ? (uint32_t)t8[u] : k;
+            const uint32_t jump = i + 1 < k && t != i + 1;
+            if (i < k) fl[i] = 0;
+            uint32_t tot;
+            const uint32_t pos = nj + block_excl<uint32_t>(jump, ws32, tot);
+            if (jump && pos < LP_JCAP) jl[pos] = i;
+            nj += tot;
+        }
     }
-    __syncthreads();
-    const uint32_t nj = nj_s;
-    uint32_t pos = wsum32[wid] + inc - cj;
-    if (nj <= LP_JCAP)
-        for (uint32_t i = b0; i < b1; i++)
-            if (i + 1 < k && tgt_of(w, i, k) != i + 1) jl[pos++] = i;
     __syncthreads();
     // B. follow the valid path over the jumpers (one warp)
     if (wid == 0) {
@@ -1063,46 +1086,43 @@ __global__ void __launch_bounds__(1024) k_lpost(Work w)
         }
     }
     __syncthreads();
-    // C. entries and valid counts, then the exclusive scan of the counts
-    uint64_t loc = 0;
-    for (uint32_t i = b0; i < b1; i++) {
-        const uint8_t f = fl[i];
-        uint64_t c = 0;
-        int64_t e = ENTRY_DEAD;
-        if (!(f & 1u)) {
-            e = i == 0 ? -1 : ((f & 2u) ? w.entry[i] : __ldcg(w.midx + i - 1));
-            SEQCDC_ASSERT((uint64_t)(e + 1) <= (__ldcg(w.Lcnt + i) & CNT_MASK));
-            c = (__ldcg(w.Lcnt + i) & CNT_MASK) - (uint64_t)(e + 1) + __ldcg(w.Xcnt + i) + __ldcg(w.cont_cnt + i);
-        }
-        w.entry[i] = e;
-        w.seg_count[i] = c;
-        loc += c;
-    }
-    uint64_t inc64 = loc;
+    // C. entries, valid counts and their exclusive scan: coalesced tiles
+    uint64_t run = 0;
+    for (uint32_t base = 0; base < k; base += LP_TILE * LP_BATCH) {
+        int64_t m8[LP_BATCH];
+        uint64_t l8[LP_BATCH];
+        uint32_t x8[LP_BATCH], c8[LP_BATCH];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint64_t t = __shfl_up_sync(FULL, inc64, o);
-        if (lane >= o) inc64 += t;
-    }
-    if (lane == 31) wsum64[wid] = inc64;
-    __syncthreads();
-    if (wid == 0) {
-        const uint64_t x = lane < (int)(nt >> 5) ? wsum64[lane] : 0;
-        uint64_t xi = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t t = __shfl_up_sync(FULL, xi, o);
-            if (lane >= o) xi += t;
+        for (uint32_t u = 0; u < LP_BATCH; u++) {
+            const uint32_t i = base + u * LP_TILE + tid;
+            const bool in = i < k;
+            m8[u] = in && i > 0 ? __ldcg(w.midx + i - 1) : -1;
+            l8[u] = in ? __ldcg(w.Lcnt + i) & CNT_MASK : 0;
+            x8[u] = in ? __ldcg(w.Xcnt + i) : 0;
+            c8[u] = in ? __ldcg(w.cont_cnt + i) : 0;
         }
-        wsum64[lane] = xi - x;
+#pragma unroll
+        for (uint32_t u = 0; u < LP_BATCH; u++) {
+            const uint32_t i = base + u * LP_TILE + tid;
+            uint64_t c = 0;
+            if (i < k) {
+                const uint8_t f = fl[i];
+                int64_t e = ENTRY_DEAD;
+                if (!(f & 1u)) {
+                    e = i == 0 ? -1 : ((f & 2u) ? w.entry[i] : m8[u]);
+                    SEQCDC_ASSERT((uint64_t)(e + 1) <= l8[u]);
+                    c = l8[u] - (uint64_t)(e + 1) + x8[u] + c8[u];
+                }
+                w.entry[i] = e;
+                w.seg_count[i] = c;
+            }
+            uint64_t tot;
+            const uint64_t ex = block_excl<uint64_t>(c, ws64, tot);
+            if (i < k) w.seg_out[i] = run + ex;
+            run += tot;
+        }
     }
-    __syncthreads();
-    uint64_t run = wsum64[wid] + inc64 - loc;
-    for (uint32_t i = b0; i < b1; i++) {
-        w.seg_out[i] = run;
-        run += w.seg_count[i];
-    }
-    if (tid == nt - 1) {
+    if (tid == 0) {
         const uint64_t total = run;
         if (w.tail_n && (fl[k - 1] & 1u)) *w.tail_n = 0;    // the last chain is not the valid one
         if (w.summary) {                                      // the overhang = the last valid cut
@@ -1125,17 +1145,6 @@ __global__ void __launch_bounds__(1024) k_lpost(Work w)
         w.cut_index[0] = 0;
         w.cut_index[1] = total;
         *w.ncuts = total;
-    }
-    if (w.push_blk) {                                         // fused exchange (as in k_post)
-        __syncthreads();
-        const uint64_t tn = w.tail_n ? min(*(volatile uint64_t *)w.tail_n, (uint64_t)w.tail_max) : 0;
-        for (uint32_t i = tid; i < 3 + tn; i += nt)
-            w.push_blk[i] = i == 0 ? w.summary[0] : i == 1 ? w.summary[1] : i == 2 ? tn : __ldcg(w.tail + (i - 3));
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence_system();
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(w.push_flag), "l"(w.push_value) : "memory");
-        }
     }
 }
 
@@ -1268,6 +1277,8 @@ struct DevInfo {
 };
 static DevInfo g_dev[64];
 static int g_last_occ;
+static int g_last_lane;            // the last single-stream call used the lane walker
+static uint32_t g_last_nseg;       // ... with this many segments
 
 static int device_info(int &sms, int &occ, int *occ_lane = nullptr)
 {
@@ -1313,10 +1324,16 @@ static bool use_lane_walker(uint64_t total, const seqcdc_params_t *p, bool singl
     const uint32_t M = p->seq_length - ((p->flags & SEQCDC_FLAG_PAIRS) ? 0u : 1u);
     if (M > 4) return false;
     const char *e = getenv("SEQCDC_WALKER");
+    if (e && !strcmp(e, "lane")) return true;
+    if (e && !strcmp(e, "warp")) return false;
+    // long chunks (max > 16 KiB) merge only after ~65+ chunks: segments would
+    // have to be far longer than the lanes allow (config 4: 4x slower)
+    if (p->max_size > 16384) return false;
     if (e && !strcmp(e, "warp")) return false;
     if (e && !strcmp(e, "lane")) return true;
-    // off by default until it beats the warp walker (profiles/r02/lane_walker.md)
-    const int mib = env_int("SEQCDC_LW_MIN_MIB", -1);
+    // it needs ~75k lanes with segments several merge distances long, i.e. a
+    // stream of tens of GiB, to beat the warp walker (profiles/r02/lane_walker.md)
+    const int mib = env_int("SEQCDC_LW_MIN_MIB", 32 << 10);
     return mib >= 0 && total >= ((uint64_t)mib << 20);
 }
 
@@ -1475,10 +1492,15 @@ static void launch_lane(const Work &w, const Plan &pl, int sms, cudaStream_t st,
     else k_lwalk<MODE, false><<<pl.walk_grid, lw::THREADS, 0, st>>>(w);
     // handed-off extensions / tail on warps, then the post; both wait on the
     // device (griddepcontrol.wait) for their predecessor: launched early
+    prof_mark(pr, 2, st);
     const void *hand = w.p.M == 4 ? (const void *)k_lhand<MODE, 4> : (const void *)k_lhand<MODE, 0>;
     launch_pdl(hand, dim3(std::max(1, sms * 16)), dim3(32), 0, st, pr == nullptr, w);
-    prof_mark(pr, 2, st);
-    launch_pdl((const void *)k_lpost, dim3(1), dim3(1024), 4 * LP_JCAP + pl.nseg1, st, pr == nullptr, w);
+    launch_pdl((const void *)k_lpost, dim3(1), dim3(512), 4 * LP_JCAP + pl.nseg1, st, pr == nullptr, w);
+    if (w.tail_max || w.push_blk) {            // range calls: the tail from the true overhang, the push
+        const void *tl = w.p.M == 4 ? (const void *)k_ltail<MODE, 4> : (const void *)k_ltail<MODE, 0>;
+        launch_pdl(tl, dim3(1), dim3(32), 0, st, pr == nullptr, w);
+        g_launches++;
+    }
     k_lcopy<<<std::max(1, sms * 8), 256, 0, st>>>(w);
     g_launches += 4;
 }
@@ -1588,7 +1610,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.X = (uint64_t *)(ws + pl.o_X);
     w.FB = (uint64_t *)(ws + pl.o_FB);
     w.hand = pl.lane ? (uint32_t *)(ws + pl.o_hand) : nullptr;
-    w.lw_ext_cap = (uint32_t)std::max(1, env_int("SEQCDC_LW_EXT_CAP", 48));
+    w.lw_ext_cap = (uint32_t)std::max(1, env_int("SEQCDC_LW_EXT_CAP", 24));
     w.cuts = d_cuts;
     w.cut_index = d_cut_index;
     w.ncuts = d_ncuts;
@@ -1655,6 +1677,8 @@ static int enqueue(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, 
     Plan pl;
     const bool lane = use_lane_walker(total, p, single_api);
     make_plan(total, ns, p, sms, occ, pl, single_api, stop, tail.max > 0, lane ? occ_lane : 0);
+    g_last_lane = lane;
+    g_last_nseg = (uint32_t)pl.nseg_max;
     const size_t extra = single_api ? SINGLE_EXTRA : 0;
     uint8_t *ws = (uint8_t *)d_ws;
     bool owned = false;
@@ -2030,9 +2054,11 @@ SEQCDC_API const char *seqcdc_build_info(void)
     int sms = 0, occ = 0, ol = 0;
     device_info(sms, occ, &ol);
     snprintf(buf, sizeof(buf),
-             "seqcdc sm_100a warp walker: cp.async ring blk=%u nblk=%u ahead=%u walkers=%dx%d (last call), "
-             "win_pairs=%u; lane walker: %u-B bulk-copy lines x2, %u-thread CTAs, %d/SM max, pf=%u; k_ext=%u",
-             BLK, NBLK, AHEAD, sms, g_last_occ, WIN_PAIRS, lw::LINE, lw::THREADS, ol, (unsigned)SEQCDC_LW_PF, K_EXT);
+             "seqcdc sm_100a; last call: %s walker, %u segments; warp walker: cp.async ring blk=%u nblk=%u "
+             "ahead=%u, %d/SM, win_pairs=%u; lane walker: %u-B cp.async lines x2 (mbarrier-polled), %u-thread "
+             "CTAs, %d/SM max, pf=%u; k_ext=%u",
+             g_last_lane ? "lane" : "warp", g_last_nseg, BLK, NBLK, AHEAD, g_last_occ, WIN_PAIRS, lw::LINE,
+             lw::THREADS, ol, (unsigned)SEQCDC_LW_PF, K_EXT);
     return buf;
 }
 

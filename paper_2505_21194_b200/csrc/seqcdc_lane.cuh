@@ -42,7 +42,7 @@ namespace lw {
 #define SEQCDC_LW_WARPS 4
 #endif
 #ifndef SEQCDC_LW_PF
-#define SEQCDC_LW_PF 64        // prefetch the next line once the scan is this far into a line
+#define SEQCDC_LW_PF 96        // prefetch the next line once the scan is this far into a line
 #endif
 
 constexpr uint32_t LSH = SEQCDC_LW_LINE_SHIFT;
@@ -641,6 +641,54 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_lhand(Work w)
         }
     }
     walker_finish(wk);
+}
+
+
+// Range calls on the lane walker, after k_lpost: if the last segment's chain
+// turned out not to be the valid one (k_lpost then zeroed tail_n), walk the
+// tail again from the true overhang (k_lpost's summary) with one warp; then
+// push the exchange block into the next range's mailbox when asked (the fused
+// exchange, as k_post does on the warp-walker path).
+template <int MODE, int MSPEC>
+__global__ void __launch_bounds__(32) k_ltail(Work w)
+{
+    __shared__ __align__(128) uint8_t ring[RING];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int lane = threadIdx.x;
+    if (w.tail_max && w.summary && *(volatile uint64_t *)w.tail_n == 0) {
+        const uint64_t abase = (uint64_t)(uintptr_t)w.in;
+        const uint64_t from = w.summary[0] - w.out_add;              // the overhang, offset into `in`
+        Walker wk;
+        walker_init(wk, ring, w.p, lane);
+        uint32_t base = walker_begin(wk, abase + from, abase + w.total);
+        const uint64_t off = wk.rb - abase;
+        ListBuf tb{0, 0};
+        if (from < w.total) {
+            lb_push(tb, from + w.out_add, w.tail, lane);
+#pragma unroll 1
+            while (tb.n < w.tail_max && base + w.p.mx <= wk.end_rel) {
+                const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+                SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
+                lb_push(tb, off + c + w.out_add, w.tail, lane);
+                base = c;
+            }
+        }
+        lb_flush(tb, w.tail, lane);
+        walker_finish(wk);
+        if (lane == 0) *w.tail_n = tb.n;
+    }
+    if (w.push_blk) {
+        __syncwarp();
+        __threadfence();
+        const uint64_t tn = w.tail_n ? min(*(volatile uint64_t *)w.tail_n, (uint64_t)w.tail_max) : 0;
+        for (uint32_t i = lane; i < 3 + tn; i += 32)
+            w.push_blk[i] = i == 0 ? w.summary[0] : i == 1 ? w.summary[1] : i == 2 ? tn : __ldcg(w.tail + (i - 3));
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(w.push_flag), "l"(w.push_value) : "memory");
+        }
+    }
 }
 
 }  // namespace seqcdc

@@ -37,9 +37,17 @@ CASES = [("uniform", 31, oracle.table1(8)), ("markov", 32, oracle.table1(4, 1)),
          ("uniform", 35, oracle.Params(0, 4, 50, 256, 4096, 16384, signed=True, pairs=True))]
 
 
+@pytest.fixture(params=["warp", "lane"])
+def walker(request, monkeypatch):
+    """Both walkers behind the range calls (the lane walker hands a range call's
+    tail to a warp: seqcdc_lane.cuh lw_serve)."""
+    monkeypatch.setenv("SEQCDC_WALKER", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("kind,seed,p", CASES)
 @pytest.mark.parametrize("G", [0, 1 << 16])
-def test_range_chunk_and_resync(kind, seed, p, G):
+def test_range_chunk_and_resync(kind, seed, p, G, walker):
     sc.set_segment_bytes(G)
     try:
         n = 6 << 20
@@ -98,6 +106,9 @@ def _free_port():
 def _worker(rank, P, port, kind, seed, n, pidx, q, comm="cpu"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if ":" in comm:                        # "<comm>:<walker>" forces the walker behind the range calls
+        comm, wk = comm.split(":")
+        os.environ["SEQCDC_WALKER"] = wk
     dist.init_process_group("gloo", rank=rank, world_size=P)
     try:
         from paper_2505_21194_b200.dist import CudaRangeBackend, Shard, chunk_sharded
@@ -139,7 +150,13 @@ SHARD_PARAMS = [oracle.table1(8), oracle.table1(4, 1), oracle.table1(16)]
                                                       (4, "zeros", 0, 5 << 20, 0, "cuda"),
                                                       (2, "markov", 45, 16 << 20, 1, "p2p"),
                                                       (3, "rampmix", 46, 24 << 20, 0, "p2p"),
-                                                      (3, "zeros", 0, 5 << 20, 0, "p2p")])
+                                                      (3, "zeros", 0, 5 << 20, 0, "p2p"),
+                                                      (8, "rampmix", 47, 24 << 20, 0, "cpu"),
+                                                      (8, "markov", 48, 24 << 20, 1, "cuda"),
+                                                      (8, "zeros", 0, 8 << 20, 0, "cuda"),
+                                                      (8, "uniform", 49, 32 << 20, 0, "p2p"),
+                                                      (3, "rampmix", 50, 24 << 20, 0, "p2p:lane"),
+                                                      (2, "markov", 51, 16 << 20, 1, "cuda:lane")])
 def test_sharded_protocol_on_one_gpu(P, kind, seed, n, pidx, comm):
     """comm="cuda": the device protocol (no host sync inside the round; the
     exchanges run on device tensors), falling back to the host loop on the
@@ -165,13 +182,13 @@ def test_sharded_protocol_on_one_gpu(P, kind, seed, n, pidx, comm):
         assert first == len(got)
         got += cuts
         assert total == want.size
-        if comm == "p2p" and kind != "zeros":   # the fused round settled it (no fallback)
+        if comm.startswith("p2p") and kind != "zeros":   # the fused round settled it (no fallback)
             assert path == "p2p", (rank, path)
     assert np.array_equal(np.asarray(got, np.uint64), want)
 
 
 @pytest.mark.parametrize("kind,seed,p", CASES)
-def test_range_tail_and_local_merge(kind, seed, p):
+def test_range_tail_and_local_merge(kind, seed, p, walker):
     """seqcdc_range_chunk_tail's tail = the oracle chain continued past the
     overhang (fully determined chunks only); seqcdc_range_merge_tail on the next
     range = the true chain of that range, whether the tail reaches the merge or
