@@ -1366,7 +1366,7 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     if (pl.lane) {
         // lane walker: one segment per lane, all lanes resident at once; the floor
         // keeps a segment several merge distances long (SURVEY.md [MC-3])
-        const uint64_t ctas = (uint64_t)std::max(1, std::min(occ_lane, env_int("SEQCDC_LW_CTAS_PER_SM", 4)));
+        const uint64_t ctas = (uint64_t)std::max(1, std::min(occ_lane, env_int("SEQCDC_LW_CTAS_PER_SM", 5)));
         const uint64_t lanes = (uint64_t)sms * ctas * lw::THREADS;
         G = std::max<uint64_t>((total + lanes - 1) / lanes,
                                (uint64_t)std::max(1, env_int("SEQCDC_LW_G_FLOOR_CHUNKS", 24)) * mx);
