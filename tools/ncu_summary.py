@@ -19,7 +19,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed_pipe_alu.sum", "smsp__inst_executed_pipe_fma.sum",
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed_pipe_uniform.sum"]
+        "sm__inst_executed_pipe_uniform.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "lts__t_requests_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
+        "lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum", "lts__t_sectors.sum"]
 
 
 def report(path, nsass=0):
@@ -41,6 +44,17 @@ def report(path, nsass=0):
                     pass
         tot = sum(x for x, _ in st) or 1
         print("  stall samples (share):", ", ".join(f"{n} {x / tot:.1%}" for x, n in sorted(st, reverse=True)[:9]))
+
+        def g(k):
+            try:
+                return float(r[h.index(k)].replace(",", ""))
+            except (ValueError, IndexError):
+                return None
+        req, sec = g("lts__t_requests_srcunit_tex_op_read.sum"), g("lts__t_sectors_srcunit_tex_op_read.sum")
+        hit = g("lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum")
+        if req and sec:
+            print(f"  L2 read sectors per request (from L1/TEX): {sec / req:.2f} (4.00 = full 128-B lines); "
+                  f"L2 read hit rate {hit / sec:.1%}" if hit is not None else "")
     if nsass:
         src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
                              capture_output=True, text=True).stdout

@@ -1,7 +1,14 @@
 #!/usr/bin/env python
-"""Single-GPU timing of the pieces of one sharded step except the NCCL
-exchanges: the speculative range pass on a 1 GiB shard (+ halo), and the
-seam re-synchronisation from a true entry (device path), as rank r > 0 does."""
+"""Single-GPU timing of the pieces of one sharded step (everything but the
+exchanges between GPUs), on rank 1's shard of a config-5-shaped stream:
+
+  python tools/range_overhead.py [SHARD_GIB ...]      (default 8 16 32)
+
+plain   = seqcdc_chunk on the shard's bytes (what one GPU would do alone)
+spec    = seqcdc_range_chunk_tail (speculative chain + the tail past the overhang)
+merge   = seqcdc_range_merge_tail with rank 0's real block (local merge)
+read    = the step's one host read (the summary row)
+One JSON line per shard size."""
 import json
 import os
 import sys
@@ -14,40 +21,51 @@ import synth  # noqa: E402
 import paper_2505_21194_b200 as sc  # noqa: E402
 from paper_2505_21194_b200.dist import CudaRangeBackend, Shard  # noqa: E402
 
-n_per = 1 << 30
-p = sc.SeqParams.table1(4, 1)
-lo = n_per                                   # rank 1 of a 1 GiB-per-rank stream
-buf = torch.empty(n_per + (CudaRangeBackend.TAIL + 1) * p.max_size, dtype=torch.uint8, device="cuda")
-synth.fill_device("markov", 2, lo, buf)
-prev = torch.empty(p.max_size * 4, dtype=torch.uint8, device="cuda")   # rank 0's tail -> its overhang
-synth.fill_device("markov", 2, lo - 2 * p.max_size, prev)
-be = CudaRangeBackend(p)
-shard = Shard(buf, n_per, lo)
-# a plausible true entry: the first cut >= lo of a chain started before lo
-full = sc.chunk(torch.cat([prev, buf[:1 << 20]]), p)
-entry = int(full[(full >= 2 * p.max_size)][0].item()) + lo - 2 * p.max_size
-d_entry = torch.tensor([entry], dtype=torch.int64, device="cuda")
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-res = []
-# the predecessor's tail block, as rank 0 would send it (its own range_chunk_tail)
-be0 = CudaRangeBackend(p)
-buf0 = torch.empty(n_per + (CudaRangeBackend.TAIL + 1) * p.max_size, dtype=torch.uint8, device="cuda")
-synth.fill_device("markov", 2, 0, buf0)
-prev = be0.spec_dev_tail(Shard(buf0, n_per, 0), last=False).extra["block"].clone()
-for it in range(8):
-    ev[0].record()
-    spec = be.spec_dev_tail(shard, last=False)
-    ev[1].record()
-    cur = be.merge_dev(shard, prev, spec)
-    ev[2].record()
-    h = cur.extra["sum3"].cpu()
-    ev[3].record()
+GiB = 1 << 30
+p = sc.SeqParams.table1(8, 0)
+halo = (CudaRangeBackend.TAIL + 1) * p.max_size
+
+
+def timed(fn, reps=5):
+    fn()
     torch.cuda.synchronize()
-    if it >= 3:
-        res.append([ev[i].elapsed_time(ev[i + 1]) for i in range(3)])
-m = [sum(r[i] for r in res) / len(res) for i in range(3)]
-st = be.status.cpu().tolist()
-print(json.dumps({"shard_bytes": n_per, "spec_with_tail_ms": round(m[0], 4), "merge_ms": round(m[1], 4),
-                  "host_read_ms": round(m[2], 4), "merged_via_tail": st[0] == 1, "tail_cuts_used": st[1],
-                  "prev_tail_n": int(prev[2].item()),
-                  "note": "plus two NCCL all_gathers per step (not measurable on one GPU)"}))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(reps):
+        fn()
+    ev[1].record()
+    torch.cuda.synchronize()
+    return ev[0].elapsed_time(ev[1]) / reps
+
+
+for gib in [int(x) for x in sys.argv[1:]] or [8, 16, 32]:
+    n_per = gib * GiB
+    buf0 = torch.empty(n_per + halo, dtype=torch.uint8, device="cuda")
+    synth.fill_device("rampmix", 5, 0, buf0)
+    buf1 = torch.empty(n_per + halo, dtype=torch.uint8, device="cuda")
+    synth.fill_device("rampmix", 5, n_per, buf1)
+    be0, be1 = CudaRangeBackend(p), CudaRangeBackend(p)
+    sh0, sh1 = Shard(buf0, n_per, 0), Shard(buf1, n_per, n_per)
+    block0 = be0.spec_dev_tail(sh0, last=False).extra["block"].clone()
+    torch.cuda.synchronize()
+    plain_cuts = torch.empty(sc.max_cuts(n_per, p), dtype=torch.int64, device="cuda")
+    plain_n = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(sc.workspace_size(n_per, 1, p), dtype=torch.uint8, device="cuda")
+    t_plain = timed(lambda: sc.chunk_into(buf1[:n_per], p, plain_cuts, plain_n, workspace=ws))
+    walker = sc.build_info().split(";")[1].strip()
+    del ws
+    spec = be1.spec_dev_tail(sh1, last=False)
+    t_spec = timed(lambda: be1.spec_dev_tail(sh1, last=False))
+    t_merge = timed(lambda: be1.merge_dev(sh1, block0, spec))
+    cur = be1.merge_dev(sh1, block0, spec)
+    t_read = timed(lambda: cur.extra["sum3"].cpu())
+    st = be1.status.cpu().tolist()
+    print(json.dumps({"shard_GiB": gib, "walker": walker, "plain_ms": round(t_plain, 4),
+                      "spec_with_tail_ms": round(t_spec, 4), "merge_ms": round(t_merge, 4),
+                      "host_read_ms": round(t_read, 4),
+                      "step_over_plain": round((t_spec + t_merge + t_read) / t_plain, 4),
+                      "merged_via_tail": st[0] == 1, "tail_n": int(be1.block[2].item()) if False else int(block0[2].item()),
+                      "note": "plus the two exchanges between GPUs (peer stores or all_gathers), not measurable here"}),
+          flush=True)
+    del buf0, buf1, be0, be1, plain_cuts
+    torch.cuda.empty_cache()
