@@ -1001,6 +1001,51 @@ __device__ __forceinline__ T block_excl(T v, T *ws, T &tot)
 
 constexpr uint32_t LP_TILE = 512, LP_BATCH = 8;   // one segment per thread per tile, 8 tiles per load round
 
+
+// Exclusive scan of LP_BATCH values per thread taken tile by tile (value u of
+// thread t is element u * blockDim + t): warp scans per tile, one combine of
+// the LP_BATCH x 16 warp totals (tile-major) by warp 0, two barriers in all.
+// Returns the prefixes in ex[], the batch total in tot.
+template <typename T>
+__device__ __forceinline__ void batch_excl(const T (&v)[LP_BATCH], T (&ex)[LP_BATCH], T *wt, T &tot)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T inc[LP_BATCH];
+#pragma unroll
+    for (uint32_t u = 0; u < LP_BATCH; u++) {
+        T x = v[u];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T t = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += t;
+        }
+        inc[u] = x;
+        if (lane == 31) wt[u * nw + wid] = x;
+    }
+    __syncthreads();
+    if (wid == 0) {                                 // tile-major exclusive scan of the warp totals
+        const uint32_t m = LP_BATCH * nw;           // <= 8 x 32
+        T carry = 0;
+        for (uint32_t b = 0; b < m; b += 32) {
+            const T x = b + lane < m ? wt[b + lane] : 0;
+            T xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const T t = __shfl_up_sync(FULL, xi, o);
+                if (lane >= o) xi += t;
+            }
+            if (b + lane < m) wt[b + lane] = carry + xi - x;
+            carry += __shfl_sync(FULL, xi, 31);
+        }
+        if (lane == 0) wt[m] = carry;
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t u = 0; u < LP_BATCH; u++) ex[u] = wt[u * nw + wid] + inc[u] - v[u];
+    tot = wt[LP_BATCH * nw];
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(512) k_lpost(Work w)
 {
     extern __shared__ __align__(128) uint8_t sm[];
@@ -1008,8 +1053,8 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
     const uint32_t k = w.nseg1;
     uint32_t *jl = (uint32_t *)sm;                 // [LP_JCAP] jumpers in ascending order
     uint8_t *fl = sm + 4 * LP_JCAP;                // [k]: bit 0 dead, bit 1 entry written by a live jumper
-    __shared__ uint32_t ws32[33];
-    __shared__ uint64_t ws64[33];
+    __shared__ uint32_t ws32[LP_BATCH * 16 + 1];
+    __shared__ uint64_t ws64[LP_BATCH * 16 + 1];
     const uint32_t tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     // A. jumpers (target != s + 1), in ascending order: coalesced tiles, order-
@@ -1022,17 +1067,19 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
             const uint32_t i = base + u * LP_TILE + tid;
             t8[u] = i < k ? __ldcg(w.target + i) : 0;
         }
+        uint32_t jp[LP_BATCH], ex[LP_BATCH], tot;
 #pragma unroll
         for (uint32_t u = 0; u < LP_BATCH; u++) {
             const uint32_t i = base + u * LP_TILE + tid;
             const uint32_t t = t8[u] >= 0 ? (uint32_t)t8[u] : k;
-            const uint32_t jump = i + 1 < k && t != i + 1;
+            jp[u] = i + 1 < k && t != i + 1;
             if (i < k) fl[i] = 0;
-            uint32_t tot;
-            const uint32_t pos = nj + block_excl<uint32_t>(jump, ws32, tot);
-            if (jump && pos < LP_JCAP) jl[pos] = i;
-            nj += tot;
         }
+        batch_excl<uint32_t>(jp, ex, ws32, tot);
+#pragma unroll
+        for (uint32_t u = 0; u < LP_BATCH; u++)
+            if (jp[u] && nj + ex[u] < LP_JCAP) jl[nj + ex[u]] = base + u * LP_TILE + tid;
+        nj += tot;
     }
     __syncthreads();
     // B. follow the valid path over the jumpers (one warp)
@@ -1101,6 +1148,7 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
             x8[u] = in ? __ldcg(w.Xcnt + i) : 0;
             c8[u] = in ? __ldcg(w.cont_cnt + i) : 0;
         }
+        uint64_t cv[LP_BATCH], ex[LP_BATCH], tot;
 #pragma unroll
         for (uint32_t u = 0; u < LP_BATCH; u++) {
             const uint32_t i = base + u * LP_TILE + tid;
@@ -1116,11 +1164,15 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
                 w.entry[i] = e;
                 w.seg_count[i] = c;
             }
-            uint64_t tot;
-            const uint64_t ex = block_excl<uint64_t>(c, ws64, tot);
-            if (i < k) w.seg_out[i] = run + ex;
-            run += tot;
+            cv[u] = c;
         }
+        batch_excl<uint64_t>(cv, ex, ws64, tot);
+#pragma unroll
+        for (uint32_t u = 0; u < LP_BATCH; u++) {
+            const uint32_t i = base + u * LP_TILE + tid;
+            if (i < k) w.seg_out[i] = run + ex[u];
+        }
+        run += tot;
     }
     if (tid == 0) {
         const uint64_t total = run;

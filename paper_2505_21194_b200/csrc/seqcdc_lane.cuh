@@ -600,38 +600,66 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
     drain(src);
     mb_inval(mb_of(src, 0));
     mb_inval(mb_of(src, 1));
-    __syncwarp();
+    {   // this warp's lanes are done and their tasks published: count them (k_lhand waits for all)
+        const uint32_t mine = __popc(__ballot_sync(FULL, s < nseg));
+        if (lane == 0 && mine) {
+            __threadfence();
+            atomicAdd(w.ctrl + C_FIN, mine);
+        }
+    }
 #ifdef SEQCDC_TIMELINE
     if (lane == 0) atomicAdd(&g_lw_stats[0], (unsigned long long)step);
 #endif
 }
 
-// The handed-off tasks, after the lane walk (stream order): persistent
-// one-warp CTAs claim tasks until none is left; then the last warp to finish
-// continues any extension on the valid path that ran out of budget (single
-// stream; as k_walk does).
+// The handed-off tasks: persistent one-warp CTAs, launched behind k_lwalk with
+// programmatic dependent launch, so they become resident only after every lane
+// CTA is, and start serving tasks as soon as lanes publish them (the lane
+// walk's tail and the hand-off work overlap).  A task index is claimed first,
+// then waited for; a warp leaves when every lane is done (k_lwalk's C_FIN) and
+// its claimed index holds no task.  The last warp to leave continues any
+// extension on the valid path that ran out of budget (single stream; as k_walk
+// does).
 template <int MODE, int MSPEC>
 __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_lhand(Work w)
 {
     __shared__ __align__(128) uint8_t ring[RING];
-    asm volatile("griddepcontrol.wait;" ::: "memory");      // the lane walk complete
-    asm volatile("griddepcontrol.launch_dependents;");
     const int lane = threadIdx.x;
+    const uint32_t nseg = w.ctrl[C_BAD] ? 0u : nseg_total(w);
     Walker wk;
     walker_init(wk, ring, w.p, lane);
-    const uint32_t ntask = *(volatile uint32_t *)(w.ctrl + C_HAND);
 #pragma unroll 1
     for (;;) {
         uint32_t j = 0;
         if (lane == 0) j = atomicAdd(w.ctrl + C_HNEXT, 1u);
         j = __shfl_sync(FULL, j, 0);
-        if (j >= ntask) break;
-        lw_serve<MODE, MSPEC>(w, wk, __ldcg(w.hand + j), lane);
+        if (j >= nseg) break;                                   // at most one task per lane
+        uint32_t task = 0;
+        if (lane == 0) {
+#pragma unroll 1
+            for (;;) {
+                task = lw::ld_acquire_u32(w.hand + j);
+                if (task) break;
+                if (lw::ld_acquire_u32(w.ctrl + C_FIN) == nseg) {   // every task is published
+                    task = lw::ld_acquire_u32(w.hand + j);
+                    if (!task) task = FULL;
+                    break;
+                }
+                __nanosleep(400);
+            }
+        }
+        task = __shfl_sync(FULL, task, 0);
+        __syncwarp();
+        if (task == FULL) break;
+        lw_serve<MODE, MSPEC>(w, wk, task, lane);
     }
+    asm volatile("griddepcontrol.launch_dependents;");
     if (w.single) {
         __syncwarp();
         uint32_t last = 0;
         if (lane == 0) {
+#pragma unroll 1
+            while (lw::ld_acquire_u32(w.ctrl + C_FIN) != nseg) __nanosleep(400);   // every lane done
             __threadfence();
             last = atomicAdd(w.ctrl + C_DONE, 1u) == gridDim.x - 1;
         }
@@ -642,7 +670,6 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_lhand(Work w)
     }
     walker_finish(wk);
 }
-
 
 // Range calls on the lane walker, after k_lpost: if the last segment's chain
 // turned out not to be the valid one (k_lpost then zeroed tail_n), walk the
