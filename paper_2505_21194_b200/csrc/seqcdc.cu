@@ -1546,11 +1546,12 @@ static void launch_lane(const Work &w, const Plan &pl, int sms, cudaStream_t st,
     // device (griddepcontrol.wait) for their predecessor: launched early
     prof_mark(pr, 2, st);
     const void *hand = w.p.M == 4 ? (const void *)k_lhand<MODE, 4> : (const void *)k_lhand<MODE, 0>;
-    launch_pdl(hand, dim3(std::max(1, sms * 16)), dim3(32), 0, st, pr == nullptr, w);
-    launch_pdl((const void *)k_lpost, dim3(1), dim3(512), 4 * LP_JCAP + pl.nseg1, st, pr == nullptr, w);
+    const bool pdl = pr == nullptr && !getenv("SEQCDC_NO_PDL");     // (debug knob: plain launches)
+    launch_pdl(hand, dim3(std::max(1, sms * 16)), dim3(32), 0, st, pdl, w);
+    launch_pdl((const void *)k_lpost, dim3(1), dim3(512), 4 * LP_JCAP + pl.nseg1, st, pdl, w);
     if (w.tail_max || w.push_blk) {            // range calls: the tail from the true overhang, the push
         const void *tl = w.p.M == 4 ? (const void *)k_ltail<MODE, 4> : (const void *)k_ltail<MODE, 0>;
-        launch_pdl(tl, dim3(1), dim3(32), 0, st, pr == nullptr, w);
+        launch_pdl(tl, dim3(1), dim3(32), 0, st, pdl, w);
         g_launches++;
     }
     k_lcopy<<<std::max(1, sms * 8), 256, 0, st>>>(w);

@@ -44,6 +44,12 @@ namespace lw {
 #ifndef SEQCDC_LW_PF
 #define SEQCDC_LW_PF 96        // prefetch the next line once the scan is this far into a line
 #endif
+#ifndef SEQCDC_LW_L2PF
+#define SEQCDC_LW_L2PF 0       // lines of the likely next anchor region warmed in L2 per chunk
+#endif
+#ifndef SEQCDC_LW_L2PF_OFF
+#define SEQCDC_LW_L2PF_OFF 0   // ... starting this many bytes past anchor + min - L
+#endif
 
 constexpr uint32_t LSH = SEQCDC_LW_LINE_SHIFT;
 constexpr uint32_t LINE = 1u << LSH;                 // bytes per bulk copy / slot
@@ -53,7 +59,7 @@ constexpr uint32_t STRIDE = 2 * LINE + 16;           // per lane: 2 slots + 16 B
 constexpr uint32_t WARPS = SEQCDC_LW_WARPS;
 constexpr uint32_t THREADS = 32 * WARPS;
 constexpr uint32_t SMEM = THREADS * STRIDE;
-static_assert(32 * STRIDE >= RING, "a finished warp's lane slots host the fallback walker's ring");
+
 static_assert(SMEM <= 48 * 1024, "static shared memory");
 static_assert(SEQCDC_LW_PF % 16 == 0 && SEQCDC_LW_PF < (int)LINE, "prefetch point inside a line");
 
@@ -212,6 +218,18 @@ __device__ __forceinline__ bool chunk_begin(Chain &c, const Src &s, const DevPar
     c.carry = 0;
     c.q = a & ~15u;
     c.la = a & 15u;
+#if SEQCDC_LW_L2PF
+    {   // the next chunk's scan most likely starts a little past a + min - L (its
+        // cut comes soon after this anchor): warm those lines in L2 now, so the
+        // dependent fill at the next anchor is an L2 hit (a guess; costs no slot)
+#pragma unroll
+        for (int k = 0; k < SEQCDC_LW_L2PF; k++) {
+            const uint32_t x = a + p.mnL + SEQCDC_LW_L2PF_OFF + k * LINE;
+            if (x + LINE <= s.end_rel)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(s.rb + x));
+        }
+    }
+#endif
     return true;
 }
 
@@ -479,6 +497,13 @@ __device__ void lw_serve(const Work &w, Walker &wk, uint32_t task, int lane)
         if ((int64_t)t != cur.t) {
             t_lo = seg_start(w, g, t);
             t_Loff = w.single ? (uint64_t)t * w.capL1 : w.Loff[t];
+            // served while lanes still walk: wait until the owning chain's list is
+            // complete (its lane never waits on a warp), so every cut is decided
+            // at once instead of being walked past
+            if (lane == 0)
+#pragma unroll 1
+                while (!(ld_acquire_u64(w.Lcnt + t) & DONE_BIT)) __nanosleep(200);
+            __syncwarp();
         }
         int64_t idx;
         if (check_cut(w, cur, t, t_lo, t_Loff, cut, idx, lane) == CK_MERGE) {

@@ -47,14 +47,21 @@ def data(n):
     return synth.fill_host(str(k), int(rng.integers(0, 1000)), int(rng.integers(0, 1 << 20)), n), str(k)
 
 
-def range_case(b, n, p):
+def range_draws(n, p):
+    """The random draws range_case makes (so a replay can skip cases)."""
+    P = int(rng.integers(2, 6))
+    R = sorted(set([0, n] + rng.integers(p.max_size, n - p.max_size, P - 1).tolist()))
+    return R
+
+
+def range_case(b, n, p, R=None):
     """The multi-GPU seam protocol emulated in one process: P contiguous ranges
     (each with its halo), speculative pass + tail per range, then in rank order
     the local merge with the previous range's tail block (when that range's
     overhang stayed speculative) or a re-walk from the true entry."""
     E = 96
-    P = int(rng.integers(2, 6))
-    R = sorted(set([0, n] + rng.integers(p.max_size, n - p.max_size, P - 1).tolist()))
+    if R is None:
+        R = range_draws(n, p)
     R = [x for i, x in enumerate(R) if i == 0 or x - R[i - 1] >= p.max_size or x == n]
     if R[-1] != n:
         R.append(n)
@@ -91,6 +98,8 @@ def range_case(b, n, p):
 
 
 t0 = time.time()
+start = int(os.environ.get("STRESS_START", "0"))      # replay: skip (draw only) the cases before it
+only = os.environ.get("STRESS_ONLY") is not None       # ... and stop after that one
 cases = cuts_checked = 0
 forms = {"single": 0, "batch": 0, "range": 0}
 while time.time() - t0 < budget:
@@ -101,6 +110,27 @@ while time.time() - t0 < budget:
     sc.set_segment_bytes(G)
     u = rng.random()
     form = "batch" if u < 0.25 else ("range" if u < 0.45 and n >= 8 * p.max_size else "single")
+    if cases < start:                            # consume exactly the draws the case would make
+        if form == "range":
+            range_draws(n, p)
+        elif form == "single":
+            rng.integers(0, 16)
+        else:
+            ns = int(rng.integers(1, 12))
+            if ns > 1:
+                rng.integers(0, n + 1, ns - 1)
+        sc.set_segment_bytes(0)
+        cases += 1
+        continue
+    if only and cases > start:
+        break
+    if os.environ.get("STRESS_DRY"):            # replay aid: leave the case for the caller
+        CASE = {"b": b, "n": n, "p": p, "kind": kind, "G": G, "form": form,
+                "R": range_draws(n, p) if form == "range" else None}
+        break
+    if os.environ.get("STRESS_LOG"):           # the case about to run (survives a crash)
+        with open(os.environ["STRESS_LOG"], "a") as f:
+            f.write(json.dumps({"case": cases, "form": form, "kind": kind, "n": n, "G": G, "params": repr(p)}) + "\n")
     try:
         if form == "range":
             got, want = range_case(b, n, p)
@@ -128,5 +158,7 @@ while time.time() - t0 < budget:
     if got.shape != want.shape or not np.array_equal(got, want):
         print(json.dumps({"mismatch": True, "form": form, "kind": kind, "n": n, "G": G, "params": repr(p)}))
         sys.exit(1)
+if os.environ.get("STRESS_DRY"):
+    sys.exit(0) if __name__ == "__main__" else None
 print(json.dumps({"stress": "ok", "cases": cases, "forms": forms, "cuts_checked": cuts_checked,
-                  "seconds": round(time.time() - t0, 1)}))
+                  "seconds": round(time.time() - t0, 1), "walker": os.environ.get("SEQCDC_WALKER", "auto")}))
