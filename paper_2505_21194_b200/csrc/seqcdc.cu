@@ -105,6 +105,9 @@ struct Work {
     // tail) are handed to warps (task list, zeroed with the control words)
     uint32_t *hand;
     uint32_t lw_ext_cap;
+    // extension budget in segments (<= K_EXT, the list capacity); a testing knob
+    // (SEQCDC_EXT_SEGS) that forces the overflow / continuation paths
+    uint32_t ext_segs;
 };
 
 struct Seg {
@@ -435,7 +438,7 @@ __device__ void walk_segment(const Work &w, Walker &wk, uint32_t s, int lane)
     int32_t tgt = TGT_OVERFLOW;
     int64_t mi = -1;
     uint64_t t_lo = 0, t_Loff = 0;
-    const uint32_t ext_end = hi_rel + (uint32_t)(K_EXT * w.G);  // byte budget (REL_CLAMP safety)
+    const uint32_t ext_end = hi_rel + (uint32_t)(w.ext_segs * w.G);  // byte budget (REL_CLAMP safety)
     // segment owning the current cut, tracked incrementally (segments are uniform
     // within a stream: segment t starts at S0 + (t - first) * G)
     uint32_t t = s;
@@ -1664,6 +1667,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.FB = (uint64_t *)(ws + pl.o_FB);
     w.hand = pl.lane ? (uint32_t *)(ws + pl.o_hand) : nullptr;
     w.lw_ext_cap = (uint32_t)std::max(1, env_int("SEQCDC_LW_EXT_CAP", 24));
+    w.ext_segs = (uint32_t)std::min<int>(K_EXT, std::max(1, env_int("SEQCDC_EXT_SEGS", (int)K_EXT)));
     w.cuts = d_cuts;
     w.cut_index = d_cut_index;
     w.ncuts = d_ncuts;

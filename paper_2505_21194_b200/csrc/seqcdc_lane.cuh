@@ -471,7 +471,7 @@ __device__ void lw_serve(const Work &w, Walker &wk, uint32_t task, int lane)
     uint32_t base = walker_begin(wk, abase + from, abase + g.E);
     const uint64_t off = wk.rb - abase;
     const uint64_t stop_abs = w.single ? w.stop : g.E;
-    const uint64_t ext_end = g.hi + K_EXT * w.G;
+    const uint64_t ext_end = g.hi + (uint64_t)w.ext_segs * w.G;
     uint32_t t = g.first + (uint32_t)((from - g.S0) / w.G);
     uint64_t t_next = seg_start(w, g, t + 1);
     Cursor cur{-1, 0, 0, 0};
@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
         c.hi_rel = g.last ? FULL : src.lo_rel + (uint32_t)(g.hi - g.lo);
         stop_abs = w.single ? w.stop : g.E;
         c.stop_rel = stop_abs - c.off < (uint64_t)FULL ? (uint32_t)(stop_abs - c.off) : FULL;
-        c.ext_end = c.hi_rel + (uint32_t)(K_EXT * w.G);
+        c.ext_end = c.hi_rel + (uint32_t)(w.ext_segs * w.G);
         c.list = w.L + g.Loff;
         c.cap = g.Lcap;
         c.n = 0;

@@ -348,3 +348,22 @@ def test_concurrent_calls_on_streams():
     want = [oracle.chunk(h, p) for h, (_, _, p) in zip(host, kinds)]
     for j, cuts, nc, _, _ in outs:
         _assert_same(cuts[: int(nc.item())].cpu().numpy(), want[j], f"stream {j}")
+
+
+@pytest.mark.parametrize("G", [1 << 14, 1 << 16])
+@pytest.mark.parametrize("kind,p", [("uniform", oracle.table1(8)), ("markov", oracle.table1(4, 1)),
+                                    ("uniform", oracle.table1(16)), ("rampmix", oracle.Params(0, 5, 103, 7, 5, 21))])
+def test_forced_overflows(G, kind, p, walker, monkeypatch):
+    """An extension budget of one segment (SEQCDC_EXT_SEGS=1, a testing knob)
+    with short segments: most extensions run out of budget, so the valid path is
+    continued by fix_overflows / k_stitch (and, on the lane walker, by the
+    hand-off warps running concurrently with the lanes); the lists must still
+    equal the oracle's.  Single stream and batch."""
+    monkeypatch.setenv("SEQCDC_EXT_SEGS", "1")
+    b = synth.fill_host(kind, 91, 0, 10 << 20)
+    sc.set_segment_bytes(G)
+    _assert_same(_gpu_chunk(b, p), oracle.chunk(b, p), f"{kind} G={G} single")
+    offs = np.array([0, 3 << 20, (3 << 20) + 12345, 10 << 20], np.uint64)
+    want_c, want_i = oracle.chunk_batch(b, offs, p)
+    got_c, got_i = _gpu_batch(b, offs, p)
+    _assert_same(got_c, want_c, f"{kind} G={G} batch")
