@@ -117,7 +117,7 @@ size_t seqcdc_workspace_size(uint64_t total_bytes, uint32_t nstreams, const seqc
  *   d_workspace/ws_bytes: optional caller scratch (see above), else NULL/0.
  * Errors: SEQCDC_EINVAL (bad params, NULL pointers with n > 0),
  * SEQCDC_ENOMEM, SEQCDC_ECUDA.
- * Walker: streams of >= 32 GiB whose runs need <= 4 favourable pairs and whose
+ * Walker: streams of >= 16 GiB whose runs need <= 4 favourable pairs and whose
  * max_size <= 16 KiB (the Table I 4/8 KiB rows) run on the per-lane sparse
  * walker, everything else on the warp walker; the environment
  * variable SEQCDC_WALKER=warp|lane forces one.  The result never depends on it.

@@ -48,15 +48,18 @@ namespace seqcdc {
 
 constexpr uint64_t DONE_BIT = 1ull << 63;
 constexpr uint64_t CNT_MASK = DONE_BIT - 1;
+constexpr uint64_t HANDED_BIT = 1ull << 62;   // lane walker: count of a speculative part a late lane handed to a warp
 constexpr int32_t TGT_END = -2;
 constexpr int32_t TGT_OVERFLOW = -3;
 constexpr int64_t ENTRY_DEAD = -2;
+constexpr int64_t ENTRY_UNSET = -3;   // k_lpost -> k_lscan: the entry follows from midx[s-1]
 constexpr uint32_t K_EXT = 8;             // extension budget, in segments
 constexpr uint64_t G_FLOOR_CHUNKS = 32;   // minimum segment length, in max_size units
 constexpr uint64_t G_CEIL = 64ull << 20;  // keeps a chain's span (G + K_EXT*G + max) far below REL_CLAMP
 constexpr uint32_t STITCH_MAX_SEGS = 8000;
 
-enum { C_NSEG = 0, C_NEXT = 1, C_BAD = 3, C_DONE = 4, C_OVF = 5, C_HAND = 6, C_HNEXT = 7, C_FIN = 8, C_NWORDS = 16 };
+enum { C_NSEG = 0, C_NEXT = 1, C_BAD = 3, C_DONE = 4, C_OVF = 5, C_HAND = 6, C_HNEXT = 7, C_FIN = 8, C_SPECDONE = 9, C_SERVED = 10,
+       C_NWORDS = 16 };
 
 struct Work {
     // inputs
@@ -104,7 +107,12 @@ struct Work {
     // lane walker: extensions longer than lw_ext_cap cuts (and a range call's
     // tail) are handed to warps (task list, zeroed with the control words)
     uint32_t *hand;
+    uint64_t *lstat;       // k_lscan tile status (look-back), zeroed with the control words
+    uint32_t *lclaim;      // per segment: a handed-off speculative part claimed by a warp (zeroed too)
     uint32_t lw_ext_cap;
+    uint32_t lw_late;      // lane walker: once this many lanes finished their speculative part, a lane
+                           // still in it hands the rest of its segment to a warp (0: never)
+    uint32_t lw_late_ext;  // ... and a lane in its extension hands that to a warp at its next cut
     // extension budget in segments (<= K_EXT, the list capacity); a testing knob
     // (SEQCDC_EXT_SEGS) that forces the overflow / continuation paths
     uint32_t ext_segs;
@@ -961,8 +969,9 @@ __global__ void __launch_bounds__(1024) k_post(Work w)
 // jumped past it; a live jumper kills the segments strictly between it and its
 // target and gives its target the entry midx[j].  Everything else is parallel.
 constexpr uint32_t LP_JCAP = 8192;                 // jumpers followed from shared memory
-constexpr uint32_t LP_MAX_SEGS = 180000;           // flags (1 B each) + jumpers fit in 227 KB
-constexpr uint32_t LP_SMEM = 4 * LP_JCAP + LP_MAX_SEGS;
+constexpr uint32_t LP_MAX_SEGS = 180000;           // (planning cap on lane-walker segments)
+constexpr uint32_t LP_SMEM = 4 * LP_JCAP;
+constexpr uint32_t LS_MAX_TILES = 64;              // >= LP_MAX_SEGS / (512 * 8)
 
 __device__ __forceinline__ uint32_t tgt_of(const Work &w, uint32_t i, uint32_t k)
 {
@@ -1055,13 +1064,11 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
     asm volatile("griddepcontrol.wait;" ::: "memory");   // the walk complete and its writes visible
     const uint32_t k = w.nseg1;
     uint32_t *jl = (uint32_t *)sm;                 // [LP_JCAP] jumpers in ascending order
-    uint8_t *fl = sm + 4 * LP_JCAP;                // [k]: bit 0 dead, bit 1 entry written by a live jumper
     __shared__ uint32_t ws32[LP_BATCH * 16 + 1];
-    __shared__ uint64_t ws64[LP_BATCH * 16 + 1];
     const uint32_t tid = threadIdx.x;
     const int lane = tid & 31, wid = tid >> 5;
     // A. jumpers (target != s + 1), in ascending order: coalesced tiles, order-
-    // preserving compaction per tile
+    // preserving compaction per tile; every entry reset to "from midx[s-1]"
     uint32_t nj = 0;
     for (uint32_t base = 0; base < k; base += LP_TILE * LP_BATCH) {
         int32_t t8[LP_BATCH];
@@ -1076,7 +1083,7 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
             const uint32_t i = base + u * LP_TILE + tid;
             const uint32_t t = t8[u] >= 0 ? (uint32_t)t8[u] : k;
             jp[u] = i + 1 < k && t != i + 1;
-            if (i < k) fl[i] = 0;
+            if (i < k) w.entry[i] = ENTRY_UNSET;
         }
         batch_excl<uint32_t>(jp, ex, ws32, tot);
 #pragma unroll
@@ -1085,7 +1092,8 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
         nj += tot;
     }
     __syncthreads();
-    // B. follow the valid path over the jumpers (one warp)
+    // B. follow the valid path over the jumpers (one warp): a live jumper's
+    // target takes its entry from the jumper, the segments in between are dead
     if (wid == 0) {
         uint32_t state = 0;                        // the next segment on the path
         if (nj <= LP_JCAP) {
@@ -1103,11 +1111,8 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
                     }
                 }
                 if ((livem >> lane) & 1u) {
-                    for (uint32_t i = j + 1; i < t && i < k; i++) fl[i] = 1;
-                    if (t < k) {
-                        fl[t] = 2;
-                        w.entry[t] = __ldcg(w.midx + j);
-                    }
+                    for (uint32_t i = j + 1; i < t && i < k; i++) w.entry[i] = ENTRY_DEAD;
+                    if (t < k) w.entry[t] = __ldcg(w.midx + j);
                 }
                 __syncwarp();
             }
@@ -1124,67 +1129,93 @@ __global__ void __launch_bounds__(512) k_lpost(Work w)
                 const uint32_t ic = cur + __ffs(nb) - 1;
                 if (ic + 1 >= k) break;
                 const uint32_t t = tgt_of(w, ic, k);
-                for (uint32_t x = ic + 1 + lane; x < t && x < k; x += 32) fl[x] = 1;
-                if (lane == 0 && t < k) {
-                    fl[t] = 2;
-                    w.entry[t] = __ldcg(w.midx + ic);
-                }
+                for (uint32_t x = ic + 1 + lane; x < t && x < k; x += 32) w.entry[x] = ENTRY_DEAD;
+                if (lane == 0 && t < k) w.entry[t] = __ldcg(w.midx + ic);
                 __syncwarp();
                 if (t >= k) break;
                 cur = t;
             }
         }
     }
-    __syncthreads();
-    // C. entries, valid counts and their exclusive scan: coalesced tiles
-    uint64_t run = 0;
-    for (uint32_t base = 0; base < k; base += LP_TILE * LP_BATCH) {
-        int64_t m8[LP_BATCH];
-        uint64_t l8[LP_BATCH];
-        uint32_t x8[LP_BATCH], c8[LP_BATCH];
+}
+
+// C. entries, valid counts and their exclusive scan, in tiles of LS_TILE
+// segments (one CTA each, all resident), chained by a decoupled look-back over
+// the tile status words (value << 2 | 1: tile total, | 2: inclusive prefix).
+// The last tile also writes the totals, the range summary and the tail check.
+constexpr uint32_t LS_TILE = LP_TILE * LP_BATCH;
+
+__global__ void __launch_bounds__(512) k_lscan(Work w)
+{
+    __shared__ uint64_t ws64[LP_BATCH * 16 + 1];
+    __shared__ uint64_t s_pre;
+    const uint32_t k = w.nseg1, tid = threadIdx.x, tile = blockIdx.x;
+    const uint32_t base = tile * LS_TILE;
+    int64_t e8[LP_BATCH], m8[LP_BATCH];
+    uint64_t l8[LP_BATCH];
+    uint32_t x8[LP_BATCH], c8[LP_BATCH];
 #pragma unroll
-        for (uint32_t u = 0; u < LP_BATCH; u++) {
-            const uint32_t i = base + u * LP_TILE + tid;
-            const bool in = i < k;
-            m8[u] = in && i > 0 ? __ldcg(w.midx + i - 1) : -1;
-            l8[u] = in ? __ldcg(w.Lcnt + i) & CNT_MASK : 0;
-            x8[u] = in ? __ldcg(w.Xcnt + i) : 0;
-            c8[u] = in ? __ldcg(w.cont_cnt + i) : 0;
-        }
-        uint64_t cv[LP_BATCH], ex[LP_BATCH], tot;
-#pragma unroll
-        for (uint32_t u = 0; u < LP_BATCH; u++) {
-            const uint32_t i = base + u * LP_TILE + tid;
-            uint64_t c = 0;
-            if (i < k) {
-                const uint8_t f = fl[i];
-                int64_t e = ENTRY_DEAD;
-                if (!(f & 1u)) {
-                    e = i == 0 ? -1 : ((f & 2u) ? w.entry[i] : m8[u]);
-                    SEQCDC_ASSERT((uint64_t)(e + 1) <= l8[u]);
-                    c = l8[u] - (uint64_t)(e + 1) + x8[u] + c8[u];
-                }
-                w.entry[i] = e;
-                w.seg_count[i] = c;
-            }
-            cv[u] = c;
-        }
-        batch_excl<uint64_t>(cv, ex, ws64, tot);
-#pragma unroll
-        for (uint32_t u = 0; u < LP_BATCH; u++) {
-            const uint32_t i = base + u * LP_TILE + tid;
-            if (i < k) w.seg_out[i] = run + ex[u];
-        }
-        run += tot;
+    for (uint32_t u = 0; u < LP_BATCH; u++) {
+        const uint32_t i = base + u * LP_TILE + tid;
+        const bool in = i < k;
+        e8[u] = in ? __ldcg(w.entry + i) : ENTRY_DEAD;
+        m8[u] = in && i > 0 ? __ldcg(w.midx + i - 1) : -1;
+        l8[u] = in ? __ldcg(w.Lcnt + i) & CNT_MASK : 0;
+        x8[u] = in ? __ldcg(w.Xcnt + i) : 0;
+        c8[u] = in ? __ldcg(w.cont_cnt + i) : 0;
     }
+    uint64_t cv[LP_BATCH], ex[LP_BATCH], tot;
+#pragma unroll
+    for (uint32_t u = 0; u < LP_BATCH; u++) {
+        const uint32_t i = base + u * LP_TILE + tid;
+        uint64_t c = 0;
+        if (i < k) {
+            int64_t e = e8[u];
+            if (e == ENTRY_UNSET) e = i == 0 ? -1 : m8[u];
+            if (e != ENTRY_DEAD) {
+                SEQCDC_ASSERT((uint64_t)(e + 1) <= l8[u]);
+                c = l8[u] - (uint64_t)(e + 1) + x8[u] + c8[u];
+            }
+            w.entry[i] = e;
+            w.seg_count[i] = c;
+        }
+        cv[u] = c;
+    }
+    batch_excl<uint64_t>(cv, ex, ws64, tot);       // (its barriers order the writes above before the publish)
     if (tid == 0) {
-        const uint64_t total = run;
-        if (w.tail_n && (fl[k - 1] & 1u)) *w.tail_n = 0;    // the last chain is not the valid one
+        __threadfence();
+        uint64_t pre = 0;
+        if (tile == 0) {
+            st_release_u64(w.lstat, (tot << 2) | 2u);
+        } else {
+            st_release_u64(w.lstat + tile, (tot << 2) | 1u);
+#pragma unroll 1
+            for (int32_t j = (int32_t)tile - 1; j >= 0; j--) {
+                uint64_t v;
+#pragma unroll 1
+                while (((v = ld_acquire_u64(w.lstat + j)) & 3u) == 0) __nanosleep(32);
+                pre += v >> 2;
+                if (v & 2u) break;
+            }
+            st_release_u64(w.lstat + tile, ((pre + tot) << 2) | 2u);
+        }
+        s_pre = pre;
+    }
+    __syncthreads();
+    const uint64_t pre = s_pre;
+#pragma unroll
+    for (uint32_t u = 0; u < LP_BATCH; u++) {
+        const uint32_t i = base + u * LP_TILE + tid;
+        if (i < k) w.seg_out[i] = pre + ex[u];
+    }
+    if (tile == gridDim.x - 1 && tid == 0) {
+        const uint64_t total = pre + tot;
+        if (w.tail_n && k && __ldcg(w.entry + k - 1) == ENTRY_DEAD) *w.tail_n = 0;   // the last chain is not the valid one
         if (w.summary) {                                      // the overhang = the last valid cut
             uint64_t ov = w.out_add;
             for (int32_t s3 = (int32_t)k - 1; s3 >= 0; s3--) {
-                if (fl[s3] & 1u) continue;
-                const int64_t e = w.entry[s3];
+                const int64_t e = __ldcg(w.entry + s3);
+                if (e == ENTRY_DEAD) continue;
                 const uint64_t nc = __ldcg(w.cont_cnt + s3), nx = __ldcg(w.Xcnt + s3);
                 const uint64_t lc = __ldcg(w.Lcnt + s3) & CNT_MASK;
                 const Seg g = get_seg(w, s3);
@@ -1387,12 +1418,18 @@ static bool use_lane_walker(uint64_t total, const seqcdc_params_t *p, bool singl
     if (e && !strcmp(e, "warp")) return false;
     if (e && !strcmp(e, "lane")) return true;
     // it needs ~75k lanes with segments several merge distances long, i.e. a
-    // stream of tens of GiB, to beat the warp walker (profiles/r02/lane_walker.md)
-    const int mib = env_int("SEQCDC_LW_MIN_MIB", 32 << 10);
+    // stream of >= 16 GiB, to beat the warp walker (profiles/r02/lane_ab_v10.jsonl:
+    // 16 GiB ramp mix 2.48 vs 2.82 ms, 8 GiB 2.21 vs 1.51 ms)
+    const int mib = env_int("SEQCDC_LW_MIN_MIB", 16 << 10);
     return mib >= 0 && total >= ((uint64_t)mib << 20);
 }
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+// lane walker: the hand-off task list (<= 2 tasks per segment), k_lscan's tile
+// status words, the claim words of handed-off speculative parts -- all zeroed
+static size_t lstat_off(uint64_t S) { return align_up(4 * (2 * S + S / 32 + 8), 8); }
+static size_t lclaim_off(uint64_t S) { return lstat_off(S) + 8 * LS_MAX_TILES; }
+static size_t lzero_end(uint64_t S) { return lclaim_off(S) + 4 * S; }
 
 static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int sms, int occ, Plan &pl,
                       bool single, uint64_t stop, bool short_tail = false, int occ_lane = 0)
@@ -1467,7 +1504,7 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
     pl.o_Lcnt = o;  // contiguous with ctrl: one memset resets both
     o = align_up(o + 8 * S, 256);
     pl.o_hand = o;  // lane walker task list, also reset by that memset
-    o = align_up(o + (pl.lane ? 4 * (S + S / 32 + 8) : 0), 256);
+    o = align_up(o + (pl.lane ? lzero_end(S) : 0), 256);
     pl.o_str_first = take(4ull * (ns + 1));
     pl.o_cont_cnt = take(4 * S);
     pl.o_seg_lo = take(single ? 0 : 8 * S);
@@ -1551,7 +1588,9 @@ static void launch_lane(const Work &w, const Plan &pl, int sms, cudaStream_t st,
     const void *hand = w.p.M == 4 ? (const void *)k_lhand<MODE, 4> : (const void *)k_lhand<MODE, 0>;
     const bool pdl = pr == nullptr && !getenv("SEQCDC_NO_PDL");     // (debug knob: plain launches)
     launch_pdl(hand, dim3(std::max(1, sms * 16)), dim3(32), 0, st, pdl, w);
-    launch_pdl((const void *)k_lpost, dim3(1), dim3(512), 4 * LP_JCAP + pl.nseg1, st, pdl, w);
+    launch_pdl((const void *)k_lpost, dim3(1), dim3(512), LP_SMEM, st, pdl, w);
+    k_lscan<<<std::max<uint32_t>(1, (pl.nseg1 + LS_TILE - 1) / LS_TILE), 512, 0, st>>>(w);
+    g_launches++;
     if (w.tail_max || w.push_blk) {            // range calls: the tail from the true overhang, the push
         const void *tl = w.p.M == 4 ? (const void *)k_ltail<MODE, 4> : (const void *)k_ltail<MODE, 0>;
         launch_pdl(tl, dim3(1), dim3(32), 0, st, pdl, w);
@@ -1666,7 +1705,15 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.X = (uint64_t *)(ws + pl.o_X);
     w.FB = (uint64_t *)(ws + pl.o_FB);
     w.hand = pl.lane ? (uint32_t *)(ws + pl.o_hand) : nullptr;
+    w.lstat = pl.lane ? (uint64_t *)(ws + pl.o_hand + lstat_off(pl.nseg_max)) : nullptr;
+    w.lclaim = pl.lane ? (uint32_t *)(ws + pl.o_hand + lclaim_off(pl.nseg_max)) : nullptr;
     w.lw_ext_cap = (uint32_t)std::max(1, env_int("SEQCDC_LW_EXT_CAP", 24));
+    {   // late lanes: after SEQCDC_LW_LATE_PCT percent of the lanes finished their speculative part
+        const int pct = env_int("SEQCDC_LW_LATE_PCT", 0);   // off: measured slower (cfg5 6.0 vs 4.9 ms at 90)
+        w.lw_late = pl.lane && pct > 0 && pct < 100 ? (uint32_t)std::max<uint64_t>(1, pl.nseg1 * (uint64_t)pct / 100) : 0;
+        const int pe = env_int("SEQCDC_LW_LATE_EXT_PCT", 0);
+        w.lw_late_ext = pl.lane && pe > 0 && pe < 100 ? (uint32_t)std::max<uint64_t>(1, pl.nseg1 * (uint64_t)pe / 100) : 0;
+    }
     w.ext_segs = (uint32_t)std::min<int>(K_EXT, std::max(1, env_int("SEQCDC_EXT_SEGS", (int)K_EXT)));
     w.cuts = d_cuts;
     w.cut_index = d_cut_index;
@@ -1690,7 +1737,7 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     }
     prof_mark(pr, 0, st);
     if (w.single) {
-        const size_t zb = pl.lane ? pl.o_hand - pl.o_ctrl + 4 * ((size_t)pl.nseg1 + pl.nseg1 / 32 + 8)
+        const size_t zb = pl.lane ? pl.o_hand - pl.o_ctrl + lzero_end(pl.nseg_max)
                                   : pl.o_Lcnt - pl.o_ctrl + 8 * pl.nseg1;
         if (cudaMemsetAsync(ws + pl.o_ctrl, 0, zb, st) != cudaSuccess)
             return SEQCDC_ECUDA;
@@ -2107,15 +2154,16 @@ SEQCDC_API const char *seqcdc_strerror(int code)
 
 SEQCDC_API const char *seqcdc_build_info(void)
 {
-    static char buf[256];
+    static char buf[320];
     int sms = 0, occ = 0, ol = 0;
     device_info(sms, occ, &ol);
     snprintf(buf, sizeof(buf),
              "seqcdc sm_100a; last call: %s walker, %u segments; warp walker: cp.async ring blk=%u nblk=%u "
-             "ahead=%u, %d/SM, win_pairs=%u; lane walker: %u-B cp.async lines x2 (mbarrier-polled), %u-thread "
-             "CTAs, %d/SM max, pf=%u; k_ext=%u",
+             "ahead=%u, %d/SM, win_pairs=%u; lane walker: %u-B %s lines x2 (mbarrier-polled%s), %u pairs/step "
+             "(%s masks), %u-thread CTAs, %d/SM max, pf=%u; k_ext=%u",
              g_last_lane ? "lane" : "warp", g_last_nseg, BLK, NBLK, AHEAD, g_last_occ, WIN_PAIRS, lw::LINE,
-             lw::THREADS, ol, (unsigned)SEQCDC_LW_PF, K_EXT);
+             SEQCDC_LW_BULK ? "cp.async.bulk" : "cp.async", SEQCDC_LW_LAZY ? " when needed" : " every step",
+             lw::GRP, SEQCDC_LW_PACKED ? "packed" : "per-word", lw::THREADS, ol, (unsigned)SEQCDC_LW_PF, K_EXT);
     return buf;
 }
 

@@ -7,21 +7,26 @@
 // it compares bytes in only 3.8% of the stream's 32-B sectors.  The warp
 // walker streams every byte through shared memory and is therefore bound by
 // HBM at ~n / 6.6 TB/s.  Here every LANE owns one speculative chain (one
-// segment) and fetches only the 128-B lines its scan touches, with 1-D bulk
-// copies (TMA, cp.async.bulk) into two private line slots, each completing on
-// its own mbarrier.  A lane whose line has not landed simply skips that loop
-// iteration (mbarrier.test_wait, no blocking), so the warp keeps scanning for
-// the lanes whose data is there; thousands of chains per SM hide the HBM
-// latency of the dependent chunk-to-chunk jumps.
+// segment) and fetches only the 128-B lines its scan touches, as 16-B
+// cp.async copies into two private line slots whose completion arrives on the
+// slot's own mbarrier (cp.async.mbarrier.arrive.noinc).  A lane whose line has
+// not landed simply skips that loop iteration (mbarrier.test_wait, no
+// blocking), so the warp keeps scanning for the lanes whose data is there;
+// thousands of chains per SM hide the HBM latency of the dependent
+// chunk-to-chunk jumps.  (Measured alternatives, profiles/r02/lane_walker.md:
+// one cp.async.bulk per line is slower -- 5.23 vs 4.37 ms on config 5 --, and
+// testing every pending slot each step costs more than testing only the slot
+// the scan needs, because every barrier test is a per-thread operation.)
 //
-// One loop iteration of a lane examines one 16-byte group: 16 byte pairs
-// (bytes q..q+16), classified with SIMD-in-word compares (4 pairs per 32-bit
-// word), the favourable-run mask by funnel-shift AND with the
-// previous group's flags, the opposing count by popc and the
-// SkipTrigger-th opposing pair by a SWAR byte select.  Decision in
-// pair order: run end first -> cut; T-th opposing pair first -> skip
-// to d+1+S with fresh counters (reading c3); neither -> next group; past
-// the limit -> forced cut.
+// One loop iteration of a lane examines one group of GRP = 32 byte pairs
+// (bytes q..q+32), classified with SIMD-in-word compares (4 pairs per 32-bit
+// word) and packed into 32-bit pair masks in pair order; the
+// favourable-run mask is an AND of shifted copies of the favourable mask with
+// the previous group's pairs shifted in, the opposing count a
+// popc, the SkipTrigger-th opposing pair a popc bisection.
+// Decision in pair order: run end first -> cut; T-th opposing pair
+// first -> skip to d+1+S with fresh counters (reading c3); neither ->
+// next group; past the limit -> forced cut.
 //
 // Segment protocol (same lists as the warp walker, so the post kernels are
 // shared): the lane records its speculative cuts < segment end in L_s and
@@ -44,6 +49,21 @@ namespace lw {
 #ifndef SEQCDC_LW_PF
 #define SEQCDC_LW_PF 96        // prefetch the next line once the scan is this far into a line
 #endif
+#ifndef SEQCDC_LW_PACKED
+#define SEQCDC_LW_PACKED 1     // packed pair masks (scan_group_p); 0: the per-word form (scan_group)
+#endif
+#ifndef SEQCDC_LW_LAZY
+#define SEQCDC_LW_LAZY 1       // test a slot's barrier only when its line is needed (barrier ops are costly)
+#endif
+#ifndef SEQCDC_LW_GROUP
+#define SEQCDC_LW_GROUP 32     // byte pairs examined per lane per step (16 or 32; 32 needs SEQCDC_LW_PACKED)
+#endif
+#ifndef SEQCDC_LW_BULK
+#define SEQCDC_LW_BULK 0       // line fills by cp.async.bulk (TMA) instead of 8 x 16-B cp.async
+#endif
+#ifndef SEQCDC_LW_ONEFILL
+#define SEQCDC_LW_ONEFILL 0    // one fill site (measured slower: 4.85 vs 4.61 ms on config 5)
+#endif
 #ifndef SEQCDC_LW_L2PF
 #define SEQCDC_LW_L2PF 0       // lines of the likely next anchor region warmed in L2 per chunk
 #endif
@@ -61,7 +81,10 @@ constexpr uint32_t THREADS = 32 * WARPS;
 constexpr uint32_t SMEM = THREADS * STRIDE;
 
 static_assert(SMEM <= 48 * 1024, "static shared memory");
-static_assert(SEQCDC_LW_PF % 16 == 0 && SEQCDC_LW_PF < (int)LINE, "prefetch point inside a line");
+constexpr uint32_t GRP = SEQCDC_LW_GROUP;             // pairs per step
+constexpr uint32_t GMASK = GRP - 1;
+static_assert(GRP == 16 || (GRP == 32 && SEQCDC_LW_PACKED), "group of 16 or (packed) 32 pairs");
+static_assert(SEQCDC_LW_PF % GRP == 0 && SEQCDC_LW_PF < (int)LINE, "prefetch point inside a line");
 
 enum { PH_SPEC = 0, PH_EXT = 1, PH_TAIL = 2, PH_DONE = 3 };
 #ifdef SEQCDC_TIMELINE
@@ -141,9 +164,16 @@ __device__ __forceinline__ void fill(Src &s, uint32_t ln)
 #endif
     if (x0 >= s.lo_rel && x0 + LINE <= s.end_rel) {
         const uint64_t src = s.rb + x0;
+#if SEQCDC_LW_BULK
+        // one bulk copy (TMA) per line: one 128-B L2 request instead of eight 16-B ones
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(LINE) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(src), "r"(LINE), "r"(mb) : "memory");
+#else
 #pragma unroll
         for (uint32_t i = 0; i < LINE; i += 16) cp_async16(dst + i, src + i);
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(mb) : "memory");
+#endif
     } else {
         // a line at the edge of the data: copy the bytes that exist, one by one
 #pragma unroll 1
@@ -188,6 +218,27 @@ __device__ __forceinline__ void request(Src &s, uint32_t ln)
     if (!((s.pend >> (ln & 1u)) & 1u)) fill(s, ln);
 }
 
+// Lazy form: a slot's barrier is tested only when its line is needed (every
+// mbarrier test is a per-thread operation of the SM's sync unit, which the
+// cp.async completions also use; testing each pending slot every step costs
+// more than the scan).  A pending slot is never refilled before it is seen
+// complete.
+__device__ __forceinline__ bool check(Src &s, uint32_t k)
+{
+    if (!((s.pend >> k) & 1u)) return true;
+    if (!mb_test(mb_of(s, k), (s.par >> k) & 1u)) return false;
+    s.pend &= ~(1u << k);
+    s.par ^= 1u << k;
+    return true;
+}
+
+__device__ __forceinline__ bool ready_lazy(Src &s, uint32_t ln) { return has(s, ln) && check(s, ln & 1u); }
+
+__device__ __forceinline__ void request_lazy(Src &s, uint32_t ln)
+{
+    if (check(s, ln & 1u)) fill(s, ln);
+}
+
 __device__ __forceinline__ uint32_t slot_addr(const Src &s, uint32_t x) { return s.sb + (x & (2 * LINE - 1)); }
 
 // ------------------------------------------------------------------ one lane's chain state
@@ -216,8 +267,8 @@ __device__ __forceinline__ bool chunk_begin(Chain &c, const Src &s, const DevPar
     if (c.limit - base < 2 || a > c.lim2) return false;
     c.need = p.T;
     c.carry = 0;
-    c.q = a & ~15u;
-    c.la = a & 15u;
+    c.q = a & ~GMASK;
+    c.la = a & GMASK;
 #if SEQCDC_LW_L2PF
     {   // the next chunk's scan most likely starts a little past a + min - L (its
         // cut comes soon after this anchor): warm those lines in L2 now, so the
@@ -311,6 +362,100 @@ __device__ __forceinline__ uint32_t scan_group(Chain &c, const Src &s, const Dev
     return NONE;
 }
 
+// ------------------------------------------------------------------ packed-mask form of the group scan
+// The same decision as scan_group, on 16-bit masks in pair order (bit i = pair
+// q+i): fewer instructions per step, and every lane of a warp runs the same
+// straight-line code.
+//
+// nib: the flag bits (bit 7 of each byte) of one word -> bits 0..3 of
+// the result in byte order; bits 4..7 are zero, bits >= 8 garbage.  With
+// w & H = sum b_k 2^(8k+7) and c = sum_j 2^(25-7j), the product's terms sit at
+// 2^(32 + 8k - 7j): k = j lands on high-word bit k, k > j at high bits >= 8, k < j
+// on six distinct low-word bits (no carries).
+__device__ __forceinline__ uint32_t nib(uint32_t w) { return __umulhi(w & H, 0x02040810u); }
+
+__device__ __forceinline__ uint32_t pack16(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3)
+{
+    const uint32_t a = __byte_perm(nib(w0), nib(w1), 0x0040);     // byte0 = n0, byte1 = n1
+    const uint32_t b = __byte_perm(nib(w2), nib(w3), 0x4000);     // byte2 = n2, byte3 = n3
+    uint32_t w = __byte_perm(a, b, 0x7610);
+    w |= w >> 4;                                                   // byte0 = n0|n1<<4, byte2 = n2|n3<<4
+    return __byte_perm(w, 0u, 0x4420);
+}
+
+// Position of the n-th (1-based) set bit of a 16-bit mask holding >= n bits.
+__device__ __forceinline__ uint32_t select16(uint32_t o, uint32_t n)
+{
+    uint32_t pos = 0, c;
+    c = __popc(o & 0xffu);
+    if (n > c) { n -= c; o >>= 8; pos += 8; }
+    c = __popc(o & 0xfu);
+    if (n > c) { n -= c; o >>= 4; pos += 4; }
+    c = __popc(o & 0x3u);
+    if (n > c) { n -= c; o >>= 2; pos += 2; }
+    if (n > (o & 1u)) pos += 1;
+    return pos;
+}
+
+__device__ __forceinline__ uint32_t select32(uint32_t o, uint32_t n)
+{
+    const uint32_t c = __popc(o & 0xffffu);
+    return n > c ? 16u + select16(o >> 16, n - c) : select16(o & 0xffffu, n);
+}
+
+template <int MODE, bool M4>
+__device__ __forceinline__ uint32_t scan_group_p(Chain &c, const Src &s, const DevParams &p)
+{
+    constexpr uint32_t XM = (MODE & 2) ? H : 0u;                      // signed reading: flip bit 7
+    constexpr int NW = GRP / 4;                                       // words of 4 pairs
+    const uint32_t q = c.q;
+    uint32_t xw[NW + 1];
+#pragma unroll
+    for (int k = 0; k < NW; k += 4) {
+        const uint4 v = lds128(slot_addr(s, q + 4 * k));
+        xw[k] = v.x ^ XM; xw[k + 1] = v.y ^ XM; xw[k + 2] = v.z ^ XM; xw[k + 3] = v.w ^ XM;
+    }
+    xw[NW] = ((q + GRP <= c.lim2 + 1) ? lds32(slot_addr(s, q + GRP)) : 0u) ^ XM;
+    uint32_t lt[NW], gt[NW];
+#pragma unroll
+    for (int k = 0; k < NW; k++) lt_gt_flags(xw[k], __funnelshift_r(xw[k], xw[k + 1], 8), lt[k], gt[k]);
+    uint32_t LT = pack16(lt[0], lt[1], lt[2], lt[3]), GT = pack16(gt[0], gt[1], gt[2], gt[3]);
+    if (GRP == 32) {
+        LT |= pack16(lt[NW - 4], lt[NW - 3], lt[NW - 2], lt[NW - 1]) << 16;
+        GT |= pack16(gt[NW - 4], gt[NW - 3], gt[NW - 2], gt[NW - 1]) << 16;
+    }
+    const uint32_t m = (GRP == 32 ? FULL : 0xffffu) << c.la;          // pairs below the anchor: not examined
+    const uint32_t F = ((MODE & 1) == 0 ? LT : GT) & m;               // favourable pairs
+    const uint32_t O = ((MODE & 1) == 0 ? GT : LT) & m;               // opposing pairs
+    // bit i of R: pairs i, i-1, ..., i-M+1 all favourable -- a run ends at pair q+i;
+    // the pairs below bit 0 are the previous group's (c.carry, zero at an anchor)
+    uint32_t R = F;
+    if (M4 || p.M > 1) R &= __funnelshift_l(c.carry, F, 1);
+    if (M4 || p.M > 2) R &= __funnelshift_l(c.carry, F, 2);
+    if (M4 || p.M > 3) R &= __funnelshift_l(c.carry, F, 3);
+    const uint32_t ctot = __popc(O);
+    if (R == 0 && ctot < c.need) {                                    // nothing decided in this group
+        c.need -= ctot;
+        c.carry = GRP == 32 ? F : F << 16;
+        c.la = 0;
+        c.q = q + GRP;
+        return q + GRP > c.lim2 ? c.limit : NONE;                     // every pair up to the limit examined
+    }
+    const uint32_t r = R ? (uint32_t)__ffs(R) - 1u : GRP;
+    if (r < GRP && (uint32_t)__popc(O & ((1u << r) - 1u)) < c.need) {   // the run completes first
+        const uint32_t pr = q + r;
+        return pr <= c.lim2 ? pr + 2 : c.limit;
+    }
+    const uint32_t pd = q + (GRP == 32 ? select32(O, c.need) : select16(O, c.need));   // skip
+    if (pd > c.lim2 || p.S >= c.lim2 - pd) return c.limit;           // lands past the limit (c8)
+    const uint32_t a = pd + 1 + p.S;                                  // reading c3
+    c.need = p.T;
+    c.carry = 0;
+    c.q = a & ~GMASK;
+    c.la = a & GMASK;
+    return NONE;
+}
+
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p)
 {
     uint32_t v;
@@ -318,13 +463,14 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p)
     return v;
 }
 
-// Publish a task for the warps (segment s's extension, or with `tail` the
-// range call's tail): its list writes are ordered before the release store.
-__device__ __forceinline__ void hand_off(const Work &w, uint32_t s, bool tail)
+// Publish a task for the warps: segment s's extension, with `tail` the range
+// call's tail, with `spec` the rest of its speculative part (then its
+// extension / tail); its list writes are ordered before the release store.
+constexpr uint32_t TASK_TAIL = 0x80000000u, TASK_SPEC = 0x40000000u, TASK_SEG = 0x3fffffffu;
+__device__ __forceinline__ void hand_off(const Work &w, uint32_t s, uint32_t kind)
 {
     const uint32_t idx = atomicAdd(w.ctrl + C_HAND, 1u);
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(w.hand + idx), "r"((s + 1) | (tail ? 0x80000000u : 0u))
-                 : "memory");
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(w.hand + idx), "r"((s + 1) | kind) : "memory");
 }
 
 // A cut of lane s's chain at relative position `cut`: record it where the
@@ -332,12 +478,13 @@ __device__ __forceinline__ void hand_off(const Work &w, uint32_t s, bool tail)
 // range tail) and decide whether the chain goes on.  Returns false when the
 // lane's work is done (its results are written).
 __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, const Seg &g, uint32_t s,
-                                       uint64_t stop_abs, uint32_t cut)
+                                       uint64_t stop_abs, uint32_t cut, bool late_ext)
 {
     const uint64_t cabs = c.off + cut;
     if (c.ph == PH_SPEC && cut >= c.hi_rel) {          // first cut past the segment: the extension starts
         TL_LANE(s, 1, 0);
         st_release_u64(w.Lcnt + s, (uint64_t)c.n | DONE_BIT);
+        if (w.lw_late || w.lw_late_ext) atomicAdd(w.ctrl + C_SPECDONE, 1u);
         c.nL = c.n;
         c.ph = PH_EXT;
         c.list = w.X + g.Xoff;
@@ -352,6 +499,7 @@ __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, 
         if (cut < c.stop_rel) return true;
         // the stream's (range's) last chunk
         st_release_u64(w.Lcnt + s, (uint64_t)c.n | DONE_BIT);
+        if (w.lw_late || w.lw_late_ext) atomicAdd(w.ctrl + C_SPECDONE, 1u);
         w.Xcnt[s] = 0;
         w.target[s] = TGT_END;
         w.midx[s] = -1;
@@ -362,7 +510,7 @@ __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, 
         }
         // range call: the chain continues past the overhang (the next rank's
         // merge) -- handed to a warp, which walks the ~100 chunks much faster
-        hand_off(w, s, true);
+        hand_off(w, s, TASK_TAIL);
         c.ph = PH_DONE;
         return false;
     }
@@ -396,17 +544,18 @@ __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, 
                     c.t_word = ld_acquire_u64(w.Lcnt + c.t);
                     if ((c.t_word & DONE_BIT) && (c.t_word & CNT_MASK)) c.cand = __ldcg(w.L + c.t_Loff + c.j);
                 }
-                if (!(c.t_word & DONE_BIT)) return true;   // not decidable yet: walk on
+                if (!(c.t_word & DONE_BIT) && !late_ext) return true;   // not decidable yet: walk on
                 const uint32_t cnt = (uint32_t)(c.t_word & CNT_MASK);
 #pragma unroll 1
-                while (c.cand < cabs && c.j + 1 < cnt) {
+                while ((c.t_word & DONE_BIT) && c.cand < cabs && c.j + 1 < cnt) {
                     c.j++;
                     c.cand = __ldcg(w.L + c.t_Loff + c.j);
                 }
-                if (c.cand != cabs) {                   // not a cut of the owning chain: walk on
-                    if (c.n < w.lw_ext_cap) return true;
+                if (!(c.t_word & DONE_BIT) || c.cand != cabs) {   // not a cut of the owning chain: walk on
+                    // (late in the walk, a warp continues the extension at once: ~30x faster per chunk)
+                    if (c.n < w.lw_ext_cap && !late_ext) return true;
                     w.Xcnt[s] = c.n;                    // a long extension: a warp continues it
-                    hand_off(w, s, false);
+                    hand_off(w, s, 0u);
                     c.ph = PH_DONE;
                     return false;
                 }
@@ -430,46 +579,114 @@ __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, 
 }  // namespace lw
 
 // A task handed off by a lane, served by a whole warp with the warp walker
-// (dense cp.async ring in the warp's idle lane slots, seqcdc_device.cuh):
-// continue segment s's extension from its last cut until a cut coincides with
-// the chain owning its region (as walk_segment's extension does), or walk a
-// range call's tail (up to tail_max cuts past the overhang, only chunks wholly
-// inside the buffer).
+// (dense cp.async ring, seqcdc_device.cuh): continue segment s's extension
+// from its last cut until a cut coincides with the chain owning its region (as
+// walk_segment's extension does), walk a range call's tail (up to tail_max
+// cuts past the overhang, only chunks wholly inside the buffer), or finish the
+// speculative part of a late lane's segment and then its extension / tail.
+
+// The range call's tail from segment s's last speculative cut (the overhang).
+template <int MODE, int MSPEC>
+__device__ void serve_tail(const Work &w, Walker &wk, uint32_t s, const Seg &g, int lane)
+{
+    const uint64_t abase = (uint64_t)(uintptr_t)w.in;
+    const uint64_t nl = __ldcg(w.Lcnt + s) & CNT_MASK;
+    const uint64_t from = __ldcg(w.L + g.Loff + nl - 1);              // the overhang
+    uint32_t base = walker_begin(wk, abase + from, abase + g.E);
+    const uint64_t off = wk.rb - abase;
+    ListBuf tb{0, 0};
+    if (base < wk.end_rel) {
+        lb_push(tb, from + w.out_add, w.tail, lane);
+#pragma unroll 1
+        while (tb.n < w.tail_max && base + w.p.mx <= wk.end_rel) {
+            const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+            SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
+            lb_push(tb, off + c + w.out_add, w.tail, lane);
+            base = c;
+        }
+    }
+    lb_flush(tb, w.tail, lane);
+    if (lane == 0) *w.tail_n = tb.n;
+}
+
+// The rest of a late lane's speculative part (its list holds >= 1 cut, count
+// published with HANDED_BIT): walk from the last cut, append the cuts inside
+// the segment, publish the list complete.  Returns true when the chain reached
+// the stream's (range's) end inside the segment -- then its bookkeeping is done
+// here, except a range call's tail.  Never waits on anything.
+template <int MODE, int MSPEC>
+__device__ bool serve_spec(const Work &w, Walker &wk, uint32_t s, const Seg &g, int lane)
+{
+    const uint64_t abase = (uint64_t)(uintptr_t)w.in;
+    uint64_t *Ls = w.L + g.Loff;
+    const uint32_t n0 = (uint32_t)(__ldcg(w.Lcnt + s) & (HANDED_BIT - 1));
+    const uint64_t from = __ldcg(Ls + n0 - 1);
+    ListBuf lb;
+    lb.n = n0;
+    lb.v = lane < (int)(n0 & 31) ? __ldcg(Ls + (n0 & ~31u) + lane) : 0;   // the open batch
+    uint32_t base = walker_begin(wk, abase + from, abase + g.E);
+    const uint64_t off = wk.rb - abase;
+    const uint64_t hi_abs = g.last ? ~0ull : g.hi;                    // (as the lane's hi_rel / stop_rel)
+    const uint64_t stop_abs = w.single ? w.stop : g.E;
+    bool end = false;
+#pragma unroll 1
+    for (;;) {
+        const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+        SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
+        const uint64_t cut = off + c;
+        if (cut >= hi_abs) break;                                     // the extension's first cut
+        SEQCDC_ASSERT(lb.n < g.Lcap);
+        lb_push(lb, cut, Ls, lane);
+        if (cut >= stop_abs) {                                        // the stream's (range's) last chunk
+            end = true;
+            break;
+        }
+        base = c;
+    }
+    lb_flush(lb, Ls, lane);
+    publish(w.Lcnt + s, lb.n, true, lane);
+    if (end && lane == 0) {
+        w.Xcnt[s] = 0;
+        w.target[s] = TGT_END;
+        w.midx[s] = -1;
+        w.cont_cnt[s] = 0;
+    }
+    __syncwarp();
+    return end;
+}
+
 template <int MODE, int MSPEC>
 __device__ void lw_serve(const Work &w, Walker &wk, uint32_t task, int lane)
 {
-    const uint32_t s = (task & 0x7fffffffu) - 1;
-    const bool tail = task >> 31;
+    const uint32_t s = (task & lw::TASK_SEG) - 1;
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
     const Seg g = get_seg(w, s);
-    if (tail) {
-        const uint64_t nl = __ldcg(w.Lcnt + s) & CNT_MASK;
-        const uint64_t from = __ldcg(w.L + g.Loff + nl - 1);          // the overhang
-        uint32_t base = walker_begin(wk, abase + from, abase + g.E);
-        const uint64_t off = wk.rb - abase;
-        ListBuf tb{0, 0};
-        if (base < wk.end_rel) {
-            lb_push(tb, from + w.out_add, w.tail, lane);
-#pragma unroll 1
-            while (tb.n < w.tail_max && base + w.p.mx <= wk.end_rel) {
-                const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
-                SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
-                lb_push(tb, off + c + w.out_add, w.tail, lane);
-                base = c;
-            }
-        }
-        lb_flush(tb, w.tail, lane);
-        if (lane == 0) *w.tail_n = tb.n;
+    if (task & lw::TASK_TAIL) {
+        serve_tail<MODE, MSPEC>(w, wk, s, g, lane);
         return;
+    }
+    if (task & lw::TASK_SPEC) {
+        uint32_t won = 0;
+        if (lane == 0) won = atomicCAS(w.lclaim + s, 0u, 1u) == 0u;
+        if (!__shfl_sync(FULL, won, 0)) return;                       // a waiting warp took it (below)
+        if (serve_spec<MODE, MSPEC>(w, wk, s, g, lane)) {
+            if (w.single && w.tail_max) serve_tail<MODE, MSPEC>(w, wk, s, g, lane);
+            return;
+        }
+        if (lane == 0) w.Xcnt[s] = 0;                                 // the extension, from the last spec cut
+        __syncwarp();
     }
     uint64_t *Xs = w.X + g.Xoff;
     const uint32_t n0 = __ldcg(w.Xcnt + s);
-    const uint64_t from = __ldcg(Xs + n0 - 1);
+    // an extension handed off by a lane continues from its last cut; one after a
+    // speculative part finished here (n0 = 0) starts at that part's last cut, so
+    // its first cut -- the first past the segment -- is walked and checked again
+    const uint64_t from = n0 ? __ldcg(Xs + n0 - 1) : __ldcg(w.L + g.Loff + ((__ldcg(w.Lcnt + s) & CNT_MASK) - 1));
     ListBuf xb;
     xb.n = n0;
     xb.v = lane < (int)(n0 & 31) ? __ldcg(Xs + (n0 & ~31u) + lane) : 0;   // the open batch
     uint32_t base = walker_begin(wk, abase + from, abase + g.E);
-    const uint64_t off = wk.rb - abase;
+    uint64_t off = wk.rb - abase;
     const uint64_t stop_abs = w.single ? w.stop : g.E;
     const uint64_t ext_end = g.hi + (uint64_t)w.ext_segs * w.G;
     uint32_t t = g.first + (uint32_t)((from - g.S0) / w.G);
@@ -480,7 +697,7 @@ __device__ void lw_serve(const Work &w, Walker &wk, uint32_t task, int lane)
     int64_t mi = -1;
 #pragma unroll 1
     for (;;) {
-        const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
+        uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
         SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
         const uint64_t cut = off + c;
         if (xb.n == g.Xcap || cut > ext_end) break;                     // budget exhausted: overflow
@@ -498,11 +715,34 @@ __device__ void lw_serve(const Work &w, Walker &wk, uint32_t task, int lane)
             t_lo = seg_start(w, g, t);
             t_Loff = w.single ? (uint64_t)t * w.capL1 : w.Loff[t];
             // served while lanes still walk: wait until the owning chain's list is
-            // complete (its lane never waits on a warp), so every cut is decided
-            // at once instead of being walked past
-            if (lane == 0)
+            // complete, so every cut is decided at once instead of being walked
+            // past.  A lane never waits on a warp; a late lane's handed-off
+            // speculative part is walked here if no warp has claimed it yet (a
+            // speculative part never waits), so no warp waits on an unserved task.
 #pragma unroll 1
-                while (!(ld_acquire_u64(w.Lcnt + t) & DONE_BIT)) __nanosleep(200);
+            for (;;) {
+                uint32_t act = 0;                                       // 0: complete, 1: wait, 2: walk it
+                if (lane == 0) {
+                    const uint64_t v = ld_acquire_u64(w.Lcnt + t);
+                    act = (v & DONE_BIT) ? 0u : ((v & HANDED_BIT) && atomicCAS(w.lclaim + t, 0u, 1u) == 0u) ? 2u : 1u;
+                }
+                act = __shfl_sync(FULL, act, 0);
+                if (act == 0) break;
+                if (act == 1) {
+                    __nanosleep(200);
+                    continue;
+                }
+                const Seg gt = get_seg(w, t);
+                if (serve_spec<MODE, MSPEC>(w, wk, t, gt, lane)) {
+                    if (lane == 0 && w.single && w.tail_max) lw::hand_off(w, t, lw::TASK_TAIL);
+                } else if (lane == 0) {
+                    w.Xcnt[t] = 0;
+                    lw::hand_off(w, t, 0u);                             // its extension: a new task
+                }
+                __syncwarp();
+                c = walker_begin(wk, abase + cut, abase + g.E);         // back to this chain
+                off = wk.rb - abase;
+            }
             __syncwarp();
         }
         int64_t idx;
@@ -582,22 +822,47 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
         }
     }
 
+#if SEQCDC_LW_LAZY
+#define REQUEST(S, L) request_lazy((S), (L))
+#else
+#define REQUEST(S, L) request((S), (L))
+#endif
     // One step of every lane per iteration, in lockstep: examine one group if
     // its lines are complete, handle a cut, keep the next lines on their way.
     uint32_t step = 0;
+    bool late = false;                                // most lanes are past their speculative part:
+    bool late_ext = false;                            // hand the rest of the segment / the extension to a warp
 #pragma unroll 1
     while (__any_sync(FULL, c.ph != PH_DONE)) {
         step++;
+        if ((w.lw_late || w.lw_late_ext) && !(late && late_ext) && (step & 31) == 0) {
+            uint32_t v = 0;
+            if (lane == 0) v = *(volatile const uint32_t *)(w.ctrl + C_SPECDONE);
+            v = __shfl_sync(FULL, v, 0);
+            late = w.lw_late && v >= w.lw_late;
+            late_ext = w.lw_late_ext && v >= w.lw_late_ext;
+        }
         if (c.ph == PH_DONE) continue;
+#if !SEQCDC_LW_LAZY
         if (src.pend) poll(src);
+#endif
         uint32_t cut = pend;
         pend = NONE;
         if (cut == NONE) {
             const uint32_t l0 = c.q >> LSH;
             // byte q+16 lies in the next line only for the line's last group
-            const bool two = (c.q & LMASK) == LINE - 16 && c.q + 16 <= c.lim2 + 1;
-            if (ready(src, l0) && (!two || ready(src, l0 + 1))) {
+            const bool two = (c.q & LMASK) == LINE - GRP && c.q + GRP <= c.lim2 + 1;
+#if SEQCDC_LW_LAZY
+            const bool ok = ready_lazy(src, l0) && (!two || ready_lazy(src, l0 + 1));
+#else
+            const bool ok = ready(src, l0) && (!two || ready(src, l0 + 1));
+#endif
+            if (ok) {
+#if SEQCDC_LW_PACKED
+                cut = scan_group_p<MODE, M4>(c, src, p);
+#else
                 cut = scan_group<MODE, M4>(c, src, p);
+#endif
 #ifdef SEQCDC_TIMELINE
                 atomicAdd(&g_lw_stats[1], 1ull);
 #endif
@@ -608,20 +873,35 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
             if (c.ph == PH_SPEC && cut < c.hi_rel && cut < c.stop_rel) {   // the common case
                 SEQCDC_ASSERT(c.n < c.cap);
                 c.list[c.n++] = c.off + cut;
-                if (!chunk_begin(c, src, p, cut)) pend = c.limit;
-            } else if (on_cut(w, c, src, g, s, stop_abs, cut)) {
+                if (late) {
+                    // a late lane: a warp walks the rest of the segment ~30x faster
+                    // (lw_serve); the count is published without DONE_BIT
+                    st_release_u64(w.Lcnt + s, (uint64_t)c.n | HANDED_BIT);
+                    hand_off(w, s, TASK_SPEC);
+                    c.ph = PH_DONE;
+                } else if (!chunk_begin(c, src, p, cut)) pend = c.limit;
+            } else if (on_cut(w, c, src, g, s, stop_abs, cut, late_ext)) {
                 if (!chunk_begin(c, src, p, cut)) pend = c.limit;
             }
         }
         if (c.ph != PH_DONE && pend == NONE) {          // the lines the next groups need, on their way
             const uint32_t l0 = c.q >> LSH;
+#if SEQCDC_LW_ONEFILL
+            // one fill site: the current line if missing, else the next once the scan is past PF
+            const uint32_t want = !has(src, l0) ? l0
+                                  : ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) &&
+                                     ((l0 + 1) << LSH) < src.end_rel) ? l0 + 1 : NONE;
+            if (want != NONE) REQUEST(src, want);
+#else
             if (!has(src, l0)) {
-                request(src, l0);
+                REQUEST(src, l0);
             } else if ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) && ((l0 + 1) << LSH) < src.end_rel) {
-                request(src, l0 + 1);
+                REQUEST(src, l0 + 1);
             }
+#endif
         }
     }
+#undef REQUEST
     drain(src);
     mb_inval(mb_of(src, 0));
     mb_inval(mb_of(src, 1));
@@ -658,14 +938,21 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_lhand(Work w)
         uint32_t j = 0;
         if (lane == 0) j = atomicAdd(w.ctrl + C_HNEXT, 1u);
         j = __shfl_sync(FULL, j, 0);
-        if (j >= nseg) break;                                   // at most one task per lane
+        if (j >= 2 * nseg + 8) break;                           // at most two tasks per segment
         uint32_t task = 0;
         if (lane == 0) {
 #pragma unroll 1
             for (;;) {
                 task = lw::ld_acquire_u32(w.hand + j);
                 if (task) break;
-                if (lw::ld_acquire_u32(w.ctrl + C_FIN) == nseg) {   // every task is published
+                // every lane done and every published task served: nobody can publish
+                // another (only a lane, or a warp serving a task, hands one off)
+                bool quiet = lw::ld_acquire_u32(w.ctrl + C_FIN) == nseg;
+                if (quiet) {                        // served first: equal counts then mean none in service
+                    const uint32_t served = lw::ld_acquire_u32(w.ctrl + C_SERVED);
+                    quiet = served == lw::ld_acquire_u32(w.ctrl + C_HAND);
+                }
+                if (quiet) {
                     task = lw::ld_acquire_u32(w.hand + j);
                     if (!task) task = FULL;
                     break;
@@ -677,6 +964,11 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_lhand(Work w)
         __syncwarp();
         if (task == FULL) break;
         lw_serve<MODE, MSPEC>(w, wk, task, lane);
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence();
+            atomicAdd(w.ctrl + C_SERVED, 1u);
+        }
     }
     asm volatile("griddepcontrol.launch_dependents;");
     if (w.single) {

@@ -18,7 +18,7 @@ import paper_2505_21194_b200 as sc  # noqa: E402
 
 GiB = 1 << 30
 which = sys.argv[1]
-n = {"cfg5": 64 * GiB, "rampmix8g": 8 * GiB, "rampmix16g": 16 * GiB, "rampmix32g": 32 * GiB}[which]
+n = {"cfg5": 64 * GiB, "rampmix8g": 8 * GiB, "rampmix12g": 12 * GiB, "rampmix16g": 16 * GiB, "rampmix32g": 32 * GiB}[which]
 d = torch.empty(n, dtype=torch.uint8, device="cuda")
 synth.fill_device("rampmix", 5, 0, d)
 p = sc.SeqParams.table1(8, 0)
