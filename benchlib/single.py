@@ -187,7 +187,7 @@ def run(args, w: Workload) -> int:
                                "by the instrumented oracle over the whole stream (SURVEY.md 8(d)); the sub-minimum "
                                "and skipped regions are never read by the method (P:179, P:189)",
             "input_rate": {"GBps": round(w.n / walk_ms / 1e6, 1), "frac": round(w.n / walk_ms / 1e6 / peak, 4),
-                           "def": "stream bytes / k_walk time (dense-equivalent rate)"},
+                           "def": f"stream bytes / {kernel} time (dense-equivalent rate)"},
             "dram_rate": ({"GBps": round(tr / walk_ms / 1e6, 1), "frac": round(tr / walk_ms / 1e6 / peak, 4),
                            "source": tr_src} if tr else None),
             "touched_fraction": chk.get("touched_fraction"),

@@ -1707,7 +1707,10 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.hand = pl.lane ? (uint32_t *)(ws + pl.o_hand) : nullptr;
     w.lstat = pl.lane ? (uint64_t *)(ws + pl.o_hand + lstat_off(pl.nseg_max)) : nullptr;
     w.lclaim = pl.lane ? (uint32_t *)(ws + pl.o_hand + lclaim_off(pl.nseg_max)) : nullptr;
-    w.lw_ext_cap = (uint32_t)std::max(1, env_int("SEQCDC_LW_EXT_CAP", 24));
+    // lane extensions longer than this many cuts go to warps: 40 for segments of
+    // >= 40 max-size chunks (config 5: 24 -> 4.94 ms, 40 -> 4.80, 64 -> 4.97), else 24
+    // (16 GiB ramp mix: 24 -> 2.51 ms, 40 -> 2.71)
+    w.lw_ext_cap = (uint32_t)std::max(1, env_int("SEQCDC_LW_EXT_CAP", pl.G >= 40ull * p->max_size ? 40 : 24));
     {   // late lanes: after SEQCDC_LW_LATE_PCT percent of the lanes finished their speculative part
         const int pct = env_int("SEQCDC_LW_LATE_PCT", 0);   // off: measured slower (cfg5 6.0 vs 4.9 ms at 90)
         w.lw_late = pl.lane && pct > 0 && pct < 100 ? (uint32_t)std::max<uint64_t>(1, pl.nseg1 * (uint64_t)pct / 100) : 0;

@@ -81,12 +81,13 @@ constexpr uint32_t AHEAD = SEQCDC_AHEAD;             // blocks kept in flight pa
 constexpr uint32_t SBLK_SHIFT = 9;                   // sparse cache: 512-byte blocks (one 16-B copy per lane)
 constexpr uint32_t SBLK = 1u << SBLK_SHIFT;
 constexpr uint32_t NS = 32;                          // sparse cache slots (16 KiB)
+constexpr uint32_t DRING = BLK * NBLK;               // dense ring: 8 KiB per walker (default geometry)
+constexpr uint32_t SRING = SBLK * NS;                // sparse block cache: 16 KiB per walker
 #if SEQCDC_SPARSE
-constexpr uint32_t RING = SBLK * NS;
+constexpr uint32_t RING = SRING;                     // the walker k_walk & co. use (build option)
 #else
-constexpr uint32_t RING = BLK * NBLK;                // 8 KiB per walker (default geometry)
+constexpr uint32_t RING = DRING;
 #endif
-constexpr uint32_t RING_MASK = RING - 1;
 static_assert(AHEAD + 2 <= NBLK, "ring must hold the window's two blocks plus the lookahead");
 static_assert(BLK >= 512 && BLK % 512 == 0, "a block is whole rounds of 32 x 16-byte copies");
 constexpr uint32_t WIN_PAIRS = 128;                  // pairs per window (32 lanes x 4)
@@ -194,7 +195,6 @@ __device__ __forceinline__ void lt_gt_flags(uint32_t x, uint32_t y, uint32_t &lt
     gt = (~y & x) | (~(x ^ y) & u);
 }
 
-#if !SEQCDC_SPARSE
 // ------------------------------------------------------------------ the shared-memory ring
 // Software-pipelined cp.async ring: BLK-byte blocks are issued strictly in order,
 // one cp.async group each; the walk keeps exactly AHEAD groups in flight past
@@ -202,7 +202,8 @@ __device__ __forceinline__ void lt_gt_flags(uint32_t x, uint32_t y, uint32_t &lt
 // AHEAD` (a constant) proves that window resident.  Block b lives in slot
 // b % NBLK; a slot is only refilled once its previous block is known to have
 // landed (else the ring drains first -- only after jumps of > NBLK-AHEAD blocks).
-struct Walker {
+struct DWalker {
+    static constexpr uint32_t BYTES = DRING, MASK = DRING - 1;
     uint64_t rb;        // absolute address of relative position 0 (RING-aligned)
     uint32_t lo_rel;    // first loadable byte (relative)
     uint32_t end_rel;   // end of the stream (relative, clamped to REL_CLAMP)
@@ -212,7 +213,7 @@ struct Walker {
 };
 
 // Issue block b (warp-uniform): one cp.async group (empty past the data).
-__device__ __forceinline__ void ring_issue(Walker &wk, uint32_t b, int lane)
+__device__ __forceinline__ void ring_issue(DWalker &wk, uint32_t b, int lane)
 {
     const uint32_t b0 = b << BLK_SHIFT;
 #if SEQCDC_L2PF > 0
@@ -226,7 +227,7 @@ __device__ __forceinline__ void ring_issue(Walker &wk, uint32_t b, int lane)
         SEQCDC_ASSERT(b0 + BLK <= REL_CLAMP);
         // a whole block: one base address per side, the k*512 steps become
         // immediate offsets of the copies (a block never wraps the ring)
-        const uint32_t dst = wk.buf + (b0 & RING_MASK) + 16 * (uint32_t)lane;
+        const uint32_t dst = wk.buf + (b0 & DWalker::MASK) + 16 * (uint32_t)lane;
         const uint64_t src = wk.rb + b0 + 16 * (uint32_t)lane;
 #pragma unroll
         for (uint32_t k = 0; k < BLK / 512; k++) cp_async16(dst + k * 512, src + k * 512);
@@ -235,12 +236,12 @@ __device__ __forceinline__ void ring_issue(Walker &wk, uint32_t b, int lane)
         for (uint32_t k = 0; k < BLK / 512; k++) {
             const uint32_t c = b0 + k * 512 + 16 * (uint32_t)lane;
             if (c >= wk.lo_rel && c + 16 <= wk.end_rel) {
-                cp_async16(wk.buf + (c & RING_MASK), wk.rb + c);
+                cp_async16(wk.buf + (c & DWalker::MASK), wk.rb + c);
             } else {
 #pragma unroll 1
                 for (uint32_t x = c; x < c + 16; x++)
                     if (x >= wk.lo_rel && x < wk.end_rel)
-                        sts8(wk.buf + (x & RING_MASK), *(const volatile uint8_t *)(wk.rb + x));
+                        sts8(wk.buf + (x & DWalker::MASK), *(const volatile uint8_t *)(wk.rb + x));
             }
         }
     }
@@ -248,7 +249,7 @@ __device__ __forceinline__ void ring_issue(Walker &wk, uint32_t b, int lane)
 }
 
 // Make bytes [need_lo, need_hi) resident (need_hi - need_lo <= BLK + 4).
-__device__ __forceinline__ void ring_need(Walker &wk, uint32_t need_lo, uint32_t need_hi, int lane)
+__device__ __forceinline__ void ring_need(DWalker &wk, uint32_t need_lo, uint32_t need_hi, int lane)
 {
     const uint32_t bw = (need_hi - 1) >> BLK_SHIFT;
     if (bw + AHEAD >= wk.b_next) {
@@ -271,7 +272,7 @@ __device__ __forceinline__ void ring_need(Walker &wk, uint32_t need_lo, uint32_t
 
 // `ring` is a static __shared__ array of RING bytes in the calling kernel (its
 // shared address is then a link-time constant).
-__device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, const DevParams &, int)
+__device__ __forceinline__ void walker_init(DWalker &wk, uint8_t *smem, const DevParams &, int)
 {
     // opaque to the compiler: kept in a register instead of being re-derived from
     // the CTA's shared window id (S2UR, long latency) at every use
@@ -285,11 +286,11 @@ __device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, const Dev
 
 // Start a job whose loadable data is absolute [a_lo, a_end); returns the
 // relative position of a_lo.  Outstanding copies of the previous job land first.
-__device__ __forceinline__ uint32_t walker_begin(Walker &wk, uint64_t a_lo, uint64_t a_end)
+__device__ __forceinline__ uint32_t walker_begin(DWalker &wk, uint64_t a_lo, uint64_t a_end)
 {
     cp_async_wait<0>();
     __syncwarp();
-    wk.rb = a_lo & ~(uint64_t)RING_MASK;
+    wk.rb = a_lo & ~(uint64_t)DWalker::MASK;
     wk.lo_rel = (uint32_t)(a_lo - wk.rb);
     const uint64_t e = a_end > a_lo ? a_end - wk.rb : wk.lo_rel;
     wk.end_rel = e > REL_CLAMP ? REL_CLAMP : (uint32_t)e;
@@ -297,15 +298,14 @@ __device__ __forceinline__ uint32_t walker_begin(Walker &wk, uint64_t a_lo, uint
     return wk.lo_rel;
 }
 
-__device__ __forceinline__ void walker_finish(Walker &wk)
+__device__ __forceinline__ void walker_finish(DWalker &wk)
 {
     cp_async_wait<0>();
     __syncwarp();
 }
 
 // (dense ring: no hint needed, the ring streams every byte)
-__device__ __forceinline__ void ring_hint_next(Walker &, uint32_t, uint32_t, int) {}
-#else
+__device__ __forceinline__ void ring_hint_next(DWalker &, uint32_t, uint32_t, int) {}
 // ------------------------------------------------------------------ sparse (skip-aware) block cache, NEXT-2
 // Instead of streaming every byte, the walker fetches only the 512-byte blocks
 // it examines, into a direct-mapped cache of NS slots (slot = block % NS), plus
@@ -314,7 +314,8 @@ __device__ __forceinline__ void ring_hint_next(Walker &, uint32_t, uint32_t, int
 // P:179).  The sub-minimum region of every chunk and most of each content-
 // defined skip are never read from HBM: this is the paper's skipping
 // turned into saved memory traffic.  Tags live one per lane (lane s = slot s).
-struct Walker {
+struct SWalker {
+    static constexpr uint32_t BYTES = SRING, MASK = SRING - 1;
     uint64_t rb;        // absolute address of relative position 0 (cache-aligned)
     uint32_t lo_rel;    // first loadable byte (relative)
     uint32_t end_rel;   // end of the stream (relative, clamped to REL_CLAMP)
@@ -325,7 +326,7 @@ struct Walker {
     uint32_t ready;     // slots known to have landed (warp-uniform bit mask)
 };
 
-__device__ __forceinline__ void cache_fill(Walker &wk, uint32_t b, int lane)
+__device__ __forceinline__ void cache_fill(SWalker &wk, uint32_t b, int lane)
 {
     const uint32_t s = b & (NS - 1);
     const uint32_t x0 = b << SBLK_SHIFT;
@@ -348,7 +349,7 @@ __device__ __forceinline__ void cache_fill(Walker &wk, uint32_t b, int lane)
 }
 
 // wait until slot s has landed (every lane committed the same groups)
-__device__ __forceinline__ void cache_wait(Walker &wk, uint32_t s)
+__device__ __forceinline__ void cache_wait(SWalker &wk, uint32_t s)
 {
     const uint32_t after = wk.gseq - 1 - __shfl_sync(FULL, wk.seq, s);   // groups committed after it
     const uint32_t n = after < 7 ? after : 7;
@@ -359,7 +360,7 @@ __device__ __forceinline__ void cache_wait(Walker &wk, uint32_t s)
 }
 
 // make block b resident (warp-uniform)
-__device__ __forceinline__ void cache_need(Walker &wk, uint32_t b, int lane)
+__device__ __forceinline__ void cache_need(SWalker &wk, uint32_t b, int lane)
 {
     const uint32_t s = b & (NS - 1);
     if (__shfl_sync(FULL, wk.tag, s) != b) cache_fill(wk, b, lane);
@@ -367,7 +368,7 @@ __device__ __forceinline__ void cache_need(Walker &wk, uint32_t b, int lane)
 }
 
 // start fetching block b unless present or its slot holds a block of the window [wl, wh]
-__device__ __forceinline__ void cache_prefetch(Walker &wk, uint32_t b, uint32_t wl, uint32_t wh, int lane)
+__device__ __forceinline__ void cache_prefetch(SWalker &wk, uint32_t b, uint32_t wl, uint32_t wh, int lane)
 {
     const uint32_t s = b & (NS - 1);
     if (b > (wk.end_rel >> SBLK_SHIFT) || ((b - wl) & (NS - 1)) <= wh - wl) return;
@@ -375,7 +376,7 @@ __device__ __forceinline__ void cache_prefetch(Walker &wk, uint32_t b, uint32_t 
 }
 
 // Make bytes [need_lo, need_hi) resident (need_hi - need_lo <= SBLK + 4).
-__device__ __forceinline__ void ring_need(Walker &wk, uint32_t need_lo, uint32_t need_hi, int lane)
+__device__ __forceinline__ void ring_need(SWalker &wk, uint32_t need_lo, uint32_t need_hi, int lane)
 {
     const uint32_t bl = need_lo >> SBLK_SHIFT, bh = (need_hi - 1) >> SBLK_SHIFT;
     cache_need(wk, bl, lane);
@@ -385,7 +386,7 @@ __device__ __forceinline__ void ring_need(Walker &wk, uint32_t need_lo, uint32_t
 }
 
 // at a chunk's first window (anchor a): prefetch where the next chunk's scan starts
-__device__ __forceinline__ void ring_hint_next(Walker &wk, uint32_t next_lo, uint32_t a, int lane)
+__device__ __forceinline__ void ring_hint_next(SWalker &wk, uint32_t next_lo, uint32_t a, int lane)
 {
     const uint32_t wl = a >> SBLK_SHIFT;
     const uint32_t b0 = next_lo >> SBLK_SHIFT;
@@ -393,7 +394,7 @@ __device__ __forceinline__ void ring_hint_next(Walker &wk, uint32_t next_lo, uin
     for (uint32_t k = 0; k < SEQCDC_HINT_BLOCKS; k++) cache_prefetch(wk, b0 + k, wl, wl + 1, lane);
 }
 
-__device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, const DevParams &, int)
+__device__ __forceinline__ void walker_init(SWalker &wk, uint8_t *smem, const DevParams &, int)
 {
     uint32_t sb = smem_u32(smem);
     asm volatile("mov.b32 %0, %0;" : "+r"(sb));
@@ -406,11 +407,11 @@ __device__ __forceinline__ void walker_init(Walker &wk, uint8_t *smem, const Dev
     wk.ready = 0;
 }
 
-__device__ __forceinline__ uint32_t walker_begin(Walker &wk, uint64_t a_lo, uint64_t a_end)
+__device__ __forceinline__ uint32_t walker_begin(SWalker &wk, uint64_t a_lo, uint64_t a_end)
 {
     cp_async_wait<0>();
     __syncwarp();
-    wk.rb = a_lo & ~(uint64_t)RING_MASK;
+    wk.rb = a_lo & ~(uint64_t)SWalker::MASK;
     wk.lo_rel = (uint32_t)(a_lo - wk.rb);
     const uint64_t e = a_end > a_lo ? a_end - wk.rb : wk.lo_rel;
     wk.end_rel = e > REL_CLAMP ? REL_CLAMP : (uint32_t)e;
@@ -419,13 +420,18 @@ __device__ __forceinline__ uint32_t walker_begin(Walker &wk, uint64_t a_lo, uint
     return wk.lo_rel;
 }
 
-__device__ __forceinline__ void walker_finish(Walker &)
+__device__ __forceinline__ void walker_finish(SWalker &)
 {
     cp_async_wait<0>();
     __syncwarp();
 }
 
+#if SEQCDC_SPARSE
+using Walker = SWalker;
+#else
+using Walker = DWalker;
 #endif
+constexpr uint32_t RING_MASK = RING - 1;
 
 // ------------------------------------------------------------------ one chunk
 // Favourable-run mask R for M = L-1 pairs.  MSPEC = 4: exactly four (L = 5,
@@ -482,8 +488,8 @@ __device__ __forceinline__ uint32_t run_mask(uint32_t Fm, uint32_t carry, uint32
 #ifndef SEQCDC_DEC_FORCE
 #define SEQCDC_DEC_FORCE -1   // tuning: 0 = ballots everywhere, 1 = REDUX everywhere
 #endif
-template <int MODE, int MSPEC, bool RED_ = true>
-__device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint32_t base, int lane)
+template <int MODE, int MSPEC, bool RED_ = true, class W = Walker>
+__device__ __forceinline__ uint32_t resolve(W &wk, const DevParams &p, uint32_t base, int lane)
 {
     constexpr bool RED = SEQCDC_DEC_FORCE < 0 ? RED_ : SEQCDC_DEC_FORCE == 1;
     uint32_t limit = base + p.mx;                  // P:266 (no overflow: base < 3 GiB, mx <= 2^28)
@@ -514,8 +520,8 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
         // MODE bit 0: Decreasing; bit 1: signed reading (flipping bit 7 of every
         // byte maps int8 order onto uint8 order)
         constexpr uint32_t XM = (MODE & 2) ? H : 0u;
-        const uint32_t x = lds32(wk.buf + (q & RING_MASK)) ^ XM;
-        const uint32_t xn = lds32(wk.buf + ((q + 4) & RING_MASK)) ^ XM;
+        const uint32_t x = lds32(wk.buf + (q & W::MASK)) ^ XM;
+        const uint32_t xn = lds32(wk.buf + ((q + 4) & W::MASK)) ^ XM;
         const uint32_t y = __funnelshift_r(x, xn, 8);     // y_k = byte q+k+1
         uint32_t lt, gt;
         lt_gt_flags(x, y, lt, gt);
@@ -565,7 +571,7 @@ __device__ __forceinline__ uint32_t resolve(Walker &wk, const DevParams &p, uint
                     const uint32_t q16 = p0 + 16 * (uint32_t)lane;
                     uint32_t wv[5];
 #pragma unroll
-                    for (int k = 0; k < 5; k++) wv[k] = lds32(wk.buf + ((q16 + 4 * k) & RING_MASK));
+                    for (int k = 0; k < 5; k++) wv[k] = lds32(wk.buf + ((q16 + 4 * k) & W::MASK));
                     uint32_t diff = 0;
 #pragma unroll
                     for (int k = 0; k < 4; k++) diff |= wv[k] ^ __funnelshift_r(wv[k], wv[k + 1], 8);

@@ -585,9 +585,34 @@ __device__ __forceinline__ bool on_cut(const Work &w, Chain &c, const Src &src, 
 // cuts past the overhang, only chunks wholly inside the buffer), or finish the
 // speculative part of a late lane's segment and then its extension / tail.
 
+#ifndef SEQCDC_LH_SPARSE
+#define SEQCDC_LH_SPARSE 0     // k_lhand's warps read sparsely (512-B block cache + next-anchor prefetch)
+#endif
+#if SEQCDC_LH_SPARSE
+using LWalker = SWalker;
+#else
+using LWalker = DWalker;
+#endif
+constexpr uint32_t LH_SMEM = LWalker::BYTES > RING ? LWalker::BYTES : RING;
+
+#ifndef SEQCDC_LH_PF
+#define SEQCDC_LH_PF 0         // lines of the next chunk's likely anchor region warmed in L2 per chunk (warps)
+#endif
+// A lone chain walked by a warp waits on memory once per chunk: the next
+// chunk's scan starts at its cut + min - L, and the cut most often
+// comes soon after this chunk's own anchor.  Warm that region in L2 while this
+// chunk is resolved (a guess; one prefetch per lane, no ring slot).
+__device__ __forceinline__ void lh_prefetch(const Work &w, uint64_t base_abs, uint64_t end_abs, int lane)
+{
+#if SEQCDC_LH_PF
+    const uint64_t x = base_abs + w.p.mn + w.p.mnL + 128u * (uint32_t)lane;
+    if (lane < SEQCDC_LH_PF && x < end_abs) asm volatile("prefetch.global.L2 [%0];" ::"l"(w.in + x));
+#endif
+}
+
 // The range call's tail from segment s's last speculative cut (the overhang).
 template <int MODE, int MSPEC>
-__device__ void serve_tail(const Work &w, Walker &wk, uint32_t s, const Seg &g, int lane)
+__device__ void serve_tail(const Work &w, LWalker &wk, uint32_t s, const Seg &g, int lane)
 {
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
     const uint64_t nl = __ldcg(w.Lcnt + s) & CNT_MASK;
@@ -599,6 +624,7 @@ __device__ void serve_tail(const Work &w, Walker &wk, uint32_t s, const Seg &g, 
         lb_push(tb, from + w.out_add, w.tail, lane);
 #pragma unroll 1
         while (tb.n < w.tail_max && base + w.p.mx <= wk.end_rel) {
+            lh_prefetch(w, off + base, g.E, lane);
             const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
             SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
             lb_push(tb, off + c + w.out_add, w.tail, lane);
@@ -615,7 +641,7 @@ __device__ void serve_tail(const Work &w, Walker &wk, uint32_t s, const Seg &g, 
 // the stream's (range's) end inside the segment -- then its bookkeeping is done
 // here, except a range call's tail.  Never waits on anything.
 template <int MODE, int MSPEC>
-__device__ bool serve_spec(const Work &w, Walker &wk, uint32_t s, const Seg &g, int lane)
+__device__ bool serve_spec(const Work &w, LWalker &wk, uint32_t s, const Seg &g, int lane)
 {
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
     uint64_t *Ls = w.L + g.Loff;
@@ -631,6 +657,7 @@ __device__ bool serve_spec(const Work &w, Walker &wk, uint32_t s, const Seg &g, 
     bool end = false;
 #pragma unroll 1
     for (;;) {
+        lh_prefetch(w, off + base, g.E, lane);
         const uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
         SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
         const uint64_t cut = off + c;
@@ -656,7 +683,7 @@ __device__ bool serve_spec(const Work &w, Walker &wk, uint32_t s, const Seg &g, 
 }
 
 template <int MODE, int MSPEC>
-__device__ void lw_serve(const Work &w, Walker &wk, uint32_t task, int lane)
+__device__ void lw_serve(const Work &w, LWalker &wk, uint32_t task, int lane)
 {
     const uint32_t s = (task & lw::TASK_SEG) - 1;
     const uint64_t abase = (uint64_t)(uintptr_t)w.in;
@@ -697,6 +724,7 @@ __device__ void lw_serve(const Work &w, Walker &wk, uint32_t task, int lane)
     int64_t mi = -1;
 #pragma unroll 1
     for (;;) {
+        lh_prefetch(w, off + base, g.E, lane);
         uint32_t c = resolve<MODE, MSPEC>(wk, w.p, base, lane);
         SEQCDC_ASSERT_CUT(base, c, w.p, wk.end_rel);
         const uint64_t cut = off + c;
@@ -928,10 +956,10 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
 template <int MODE, int MSPEC>
 __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_lhand(Work w)
 {
-    __shared__ __align__(128) uint8_t ring[RING];
+    __shared__ __align__(128) uint8_t ring[LH_SMEM];
     const int lane = threadIdx.x;
     const uint32_t nseg = w.ctrl[C_BAD] ? 0u : nseg_total(w);
-    Walker wk;
+    LWalker wk;
     walker_init(wk, ring, w.p, lane);
 #pragma unroll 1
     for (;;) {
@@ -982,7 +1010,13 @@ __global__ void __launch_bounds__(32, SEQCDC_MIN_BLOCKS) k_lhand(Work w)
         }
         if (__shfl_sync(FULL, last, 0)) {
             __threadfence();
-            if (*(volatile uint32_t *)(w.ctrl + C_OVF)) fix_overflows<MODE, MSPEC>(w, wk, lane);
+            if (*(volatile uint32_t *)(w.ctrl + C_OVF)) {
+                walker_finish(wk);
+                Walker fw;                              // the library's walker, on the same shared memory
+                walker_init(fw, ring, w.p, lane);
+                fix_overflows<MODE, MSPEC>(w, fw, lane);
+                walker_finish(fw);
+            }
         }
     }
     walker_finish(wk);
