@@ -1313,7 +1313,8 @@ struct Plan {
     size_t o_ctrl, o_Lcnt, o_str_first, o_cont_cnt, o_seg_lo, o_seg_hi, o_seg_stream, o_Loff, o_Xoff,
         o_Lcap, o_Xcap, o_Xcnt, o_target, o_midx, o_entry, o_seg_count, o_seg_out, o_L, o_X, o_FB, o_hand;
     uint32_t walk_grid;
-    bool lane;             // single stream on the lane walker (k_lwalk + k_lpost + k_lcopy)
+    bool lane;             // single stream on the lane walker (k_lwalk + k_lpost + k_lscan + k_lcopy)
+    uint64_t lane_slots;   // lanes the lane walker could run (SMs x CTAs x threads)
 };
 
 static std::atomic<uint64_t> g_launches{0};   // kernels this library has launched (process-wide)
@@ -1460,6 +1461,7 @@ static void make_plan(uint64_t total, uint32_t ns, const seqcdc_params_t *p, int
         // keeps a segment several merge distances long (SURVEY.md [MC-3])
         const uint64_t ctas = (uint64_t)std::max(1, std::min(occ_lane, env_int("SEQCDC_LW_CTAS_PER_SM", 5)));
         const uint64_t lanes = (uint64_t)sms * ctas * lw::THREADS;
+        pl.lane_slots = lanes;
         G = std::max<uint64_t>((total + lanes - 1) / lanes,
                                (uint64_t)std::max(1, env_int("SEQCDC_LW_G_FLOOR_CHUNKS", 24)) * mx);
         G = std::max<uint64_t>(G, (total + LP_MAX_SEGS - 3) / (LP_MAX_SEGS - 2));
@@ -1707,10 +1709,12 @@ static int run(const uint8_t *d_in, const uint64_t *d_offsets, uint32_t ns, uint
     w.hand = pl.lane ? (uint32_t *)(ws + pl.o_hand) : nullptr;
     w.lstat = pl.lane ? (uint64_t *)(ws + pl.o_hand + lstat_off(pl.nseg_max)) : nullptr;
     w.lclaim = pl.lane ? (uint32_t *)(ws + pl.o_hand + lclaim_off(pl.nseg_max)) : nullptr;
-    // lane extensions longer than this many cuts go to warps: 40 for segments of
-    // >= 40 max-size chunks (config 5: 24 -> 4.94 ms, 40 -> 4.80, 64 -> 4.97), else 24
-    // (16 GiB ramp mix: 24 -> 2.51 ms, 40 -> 2.71)
-    w.lw_ext_cap = (uint32_t)std::max(1, env_int("SEQCDC_LW_EXT_CAP", pl.G >= 40ull * p->max_size ? 40 : 24));
+    // lane extensions longer than this many cuts go to warps: 40 when the segments
+    // fill (>= 3/4 of) the lane slots (config 5: 24 -> 4.94 ms, 40 -> 4.80, 64 -> 4.97;
+    // 32 GiB ramp mix: 24 -> 3.49, 40 -> 3.38), else 24 (16 GiB, 46% of the slots:
+    // 24 -> 2.51 ms, 40 -> 2.71)
+    w.lw_ext_cap = (uint32_t)std::max(
+        1, env_int("SEQCDC_LW_EXT_CAP", pl.lane && 4ull * pl.nseg1 >= 3ull * pl.lane_slots ? 40 : 24));
     {   // late lanes: after SEQCDC_LW_LATE_PCT percent of the lanes finished their speculative part
         const int pct = env_int("SEQCDC_LW_LATE_PCT", 0);   // off: measured slower (cfg5 6.0 vs 4.9 ms at 90)
         w.lw_late = pl.lane && pct > 0 && pct < 100 ? (uint32_t)std::max<uint64_t>(1, pl.nseg1 * (uint64_t)pct / 100) : 0;
