@@ -367,3 +367,23 @@ def test_forced_overflows(G, kind, p, walker, monkeypatch):
     want_c, want_i = oracle.chunk_batch(b, offs, p)
     got_c, got_i = _gpu_batch(b, offs, p)
     _assert_same(got_c, want_c, f"{kind} G={G} batch")
+
+
+@pytest.mark.parametrize("knobs", [{"SEQCDC_LW_LATE_PCT": "50"}, {"SEQCDC_LW_LATE_EXT_PCT": "50"},
+                                   {"SEQCDC_LW_LATE_PCT": "10", "SEQCDC_LW_LATE_EXT_PCT": "10", "SEQCDC_LW_EXT_CAP": "4"}])
+@pytest.mark.parametrize("G", [1 << 16, 1 << 18])
+@pytest.mark.parametrize("kind,p", [("rampmix", oracle.table1(8)), ("markov", oracle.table1(4, 1)),
+                                    ("uniform", oracle.table1(4))])
+def test_lane_late_handoffs(knobs, G, kind, p, monkeypatch):
+    """The lane walker's optional late hand-offs (off by default, measured
+    slower): once a share of the lanes finished their speculative part, a lane
+    still in it hands the rest of its segment to a warp (lw_serve's TASK_SPEC,
+    claimed by a queue warp or by a warp waiting on that segment), and a lane in
+    its extension hands that over at its next cut.  The cut lists must still
+    equal the oracle's."""
+    monkeypatch.setenv("SEQCDC_WALKER", "lane")
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    b = synth.fill_host(kind, 93, 0, 12 << 20)
+    sc.set_segment_bytes(G)
+    _assert_same(_gpu_chunk(b, p), oracle.chunk(b, p), f"{kind} G={G} {knobs}")
