@@ -58,6 +58,9 @@ namespace lw {
 #ifndef SEQCDC_LW_GROUP
 #define SEQCDC_LW_GROUP 32     // byte pairs examined per lane per step (16 or 32; 32 needs SEQCDC_LW_PACKED)
 #endif
+#ifndef SEQCDC_LW_BATCH
+#define SEQCDC_LW_BATCH 0      // fills of one warp step complete on one of 8 per-warp barriers (no per-lane arrive loop)
+#endif
 #ifndef SEQCDC_LW_BULK
 #define SEQCDC_LW_BULK 0       // line fills by cp.async.bulk (TMA) instead of 8 x 16-B cp.async
 #endif
@@ -78,7 +81,9 @@ constexpr uint32_t STRIDE = 2 * LINE + 16;           // per lane: 2 slots + 16 B
                                                      // the 8 lanes of each LDS.128 phase on distinct banks
 constexpr uint32_t WARPS = SEQCDC_LW_WARPS;
 constexpr uint32_t THREADS = 32 * WARPS;
-constexpr uint32_t SMEM = THREADS * STRIDE;
+constexpr uint32_t NBATCH = 8;                       // per-warp batch barriers (SEQCDC_LW_BATCH)
+constexpr uint32_t SMEM_LANES = THREADS * STRIDE;
+constexpr uint32_t SMEM = SMEM_LANES + (SEQCDC_LW_BATCH ? WARPS * NBATCH * 8 : 0);
 
 static_assert(SMEM <= 48 * 1024, "static shared memory");
 constexpr uint32_t GRP = SEQCDC_LW_GROUP;             // pairs per step
@@ -131,6 +136,8 @@ struct Src {
     uint32_t tag0, tag1; // line held (or being filled) by each slot (NONE: none)
     uint32_t pend;       // bit k: slot k's fill not yet seen complete
     uint32_t par;        // bit k: parity slot k's barrier completes next
+    uint32_t bsel;       // (SEQCDC_LW_BATCH) bits 4k..4k+3: slot k's batch barrier (3 bits) and phase parity
+    uint32_t wb;         // (SEQCDC_LW_BATCH) shared address of this warp's batch barriers
 };
 
 __device__ __forceinline__ uint32_t mb_of(const Src &s, uint32_t k) { return s.sb + 2 * LINE + 8 * k; }
@@ -237,6 +244,43 @@ __device__ __forceinline__ bool ready_lazy(Src &s, uint32_t ln) { return has(s, 
 __device__ __forceinline__ void request_lazy(Src &s, uint32_t ln)
 {
     if (check(s, ln & 1u)) fill(s, ln);
+}
+
+// Batch form (SEQCDC_LW_BATCH): the lanes that fill in one warp step all arrive
+// on the same per-warp barrier (a warp-uniform address: one arrive instruction
+// instead of a loop over the filling lanes' own barriers); a slot remembers
+// its batch barrier and phase.  A batch barrier is re-armed only once its
+// previous phase completed, so a recorded phase can never be confused.
+__device__ __forceinline__ bool check_b(Src &s, uint32_t k)
+{
+    if (!((s.pend >> k) & 1u)) return true;
+    const uint32_t bs = (s.bsel >> (4 * k)) & 0xfu;
+    if (!mb_test(s.wb + 8 * (bs & 7u), bs >> 3)) return false;
+    s.pend &= ~(1u << k);
+    return true;
+}
+
+__device__ __forceinline__ void fill_b(Src &s, uint32_t ln, uint32_t mb, uint32_t kb, uint32_t par)
+{
+    const uint32_t k = ln & 1u;
+    const uint32_t dst = s.sb + k * LINE;
+    const uint32_t x0 = ln << LSH;
+    if (x0 >= s.lo_rel && x0 + LINE <= s.end_rel) {
+        const uint64_t src = s.rb + x0;
+#pragma unroll
+        for (uint32_t i = 0; i < LINE; i += 16) cp_async16(dst + i, src + i);
+        asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(mb) : "memory");   // pending +1
+        s.pend |= 1u << k;
+        s.bsel = (s.bsel & ~(0xfu << (4 * k))) | ((kb | (par << 3)) << (4 * k));
+    } else {
+        // a line at the edge of the data: copied here, complete at once (only this lane reads it)
+#pragma unroll 1
+        for (uint32_t i = 0; i < LINE; i++) {
+            const uint32_t x = x0 + i;
+            if (x >= s.lo_rel && x < s.end_rel) sts8(dst + i, *(const volatile uint8_t *)(s.rb + x));
+        }
+    }
+    if (k) s.tag1 = ln; else s.tag0 = ln;
 }
 
 __device__ __forceinline__ uint32_t slot_addr(const Src &s, uint32_t x) { return s.sb + (x & (2 * LINE - 1)); }
@@ -811,8 +855,16 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
         asm volatile("mov.b32 %0, %0;" : "+r"(sb));
         src.sb = sb;
     }
+#if SEQCDC_LW_BATCH
+    src.wb = smem_u32(sm) + SMEM_LANES + (threadIdx.x >> 5) * NBATCH * 8;
+    if (lane < (int)NBATCH) mb_init(src.wb + 8 * lane);
+    __syncwarp();
+    src.bsel = 0;
+    uint32_t wnext = 0, wpar = 0, wused = 0;          // warp-uniform: next batch barrier, phase parities, armed
+#else
     mb_init(mb_of(src, 0));
     mb_init(mb_of(src, 1));
+#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     src.tag0 = src.tag1 = NONE;
     src.pend = src.par = 0;
@@ -870,69 +922,111 @@ __global__ void __launch_bounds__(lw::THREADS) k_lwalk(Work w)
             late = w.lw_late && v >= w.lw_late;
             late_ext = w.lw_late_ext && v >= w.lw_late_ext;
         }
-        if (c.ph == PH_DONE) continue;
-#if !SEQCDC_LW_LAZY
-        if (src.pend) poll(src);
+        uint32_t want = NONE;                           // (batch form) the line this lane asks for
+        if (c.ph != PH_DONE) {
+#if !SEQCDC_LW_LAZY && !SEQCDC_LW_BATCH
+            if (src.pend) poll(src);
 #endif
-        uint32_t cut = pend;
-        pend = NONE;
-        if (cut == NONE) {
-            const uint32_t l0 = c.q >> LSH;
-            // byte q+16 lies in the next line only for the line's last group
-            const bool two = (c.q & LMASK) == LINE - GRP && c.q + GRP <= c.lim2 + 1;
-#if SEQCDC_LW_LAZY
-            const bool ok = ready_lazy(src, l0) && (!two || ready_lazy(src, l0 + 1));
+            uint32_t cut = pend;
+            pend = NONE;
+            if (cut == NONE) {
+                const uint32_t l0 = c.q >> LSH;
+                // byte q+GRP lies in the next line only for the line's last group
+                const bool two = (c.q & LMASK) == LINE - GRP && c.q + GRP <= c.lim2 + 1;
+#if SEQCDC_LW_BATCH
+                const bool ok = has(src, l0) && check_b(src, l0 & 1u) &&
+                                (!two || (has(src, l0 + 1) && check_b(src, (l0 + 1) & 1u)));
+#elif SEQCDC_LW_LAZY
+                const bool ok = ready_lazy(src, l0) && (!two || ready_lazy(src, l0 + 1));
 #else
-            const bool ok = ready(src, l0) && (!two || ready(src, l0 + 1));
+                const bool ok = ready(src, l0) && (!two || ready(src, l0 + 1));
 #endif
-            if (ok) {
+                if (ok) {
 #if SEQCDC_LW_PACKED
-                cut = scan_group_p<MODE, M4>(c, src, p);
+                    cut = scan_group_p<MODE, M4>(c, src, p);
 #else
-                cut = scan_group<MODE, M4>(c, src, p);
+                    cut = scan_group<MODE, M4>(c, src, p);
 #endif
 #ifdef SEQCDC_TIMELINE
-                atomicAdd(&g_lw_stats[1], 1ull);
+                    atomicAdd(&g_lw_stats[1], 1ull);
 #endif
+                }
             }
-        }
-        if (cut != NONE) {
-            SEQCDC_ASSERT_CUT(c.base, cut, p, src.end_rel);
-            if (c.ph == PH_SPEC && cut < c.hi_rel && cut < c.stop_rel) {   // the common case
-                SEQCDC_ASSERT(c.n < c.cap);
-                c.list[c.n++] = c.off + cut;
-                if (late) {
-                    // a late lane: a warp walks the rest of the segment ~30x faster
-                    // (lw_serve); the count is published without DONE_BIT
-                    st_release_u64(w.Lcnt + s, (uint64_t)c.n | HANDED_BIT);
-                    hand_off(w, s, TASK_SPEC);
-                    c.ph = PH_DONE;
-                } else if (!chunk_begin(c, src, p, cut)) pend = c.limit;
-            } else if (on_cut(w, c, src, g, s, stop_abs, cut, late_ext)) {
-                if (!chunk_begin(c, src, p, cut)) pend = c.limit;
+            if (cut != NONE) {
+                SEQCDC_ASSERT_CUT(c.base, cut, p, src.end_rel);
+                if (c.ph == PH_SPEC && cut < c.hi_rel && cut < c.stop_rel) {   // the common case
+                    SEQCDC_ASSERT(c.n < c.cap);
+                    c.list[c.n++] = c.off + cut;
+                    if (late) {
+                        // a late lane: a warp walks the rest of the segment ~30x faster
+                        // (lw_serve); the count is published without DONE_BIT
+                        st_release_u64(w.Lcnt + s, (uint64_t)c.n | HANDED_BIT);
+                        hand_off(w, s, TASK_SPEC);
+                        c.ph = PH_DONE;
+                    } else if (!chunk_begin(c, src, p, cut)) pend = c.limit;
+                } else if (on_cut(w, c, src, g, s, stop_abs, cut, late_ext)) {
+                    if (!chunk_begin(c, src, p, cut)) pend = c.limit;
+                }
             }
-        }
-        if (c.ph != PH_DONE && pend == NONE) {          // the lines the next groups need, on their way
-            const uint32_t l0 = c.q >> LSH;
-#if SEQCDC_LW_ONEFILL
-            // one fill site: the current line if missing, else the next once the scan is past PF
-            const uint32_t want = !has(src, l0) ? l0
-                                  : ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) &&
-                                     ((l0 + 1) << LSH) < src.end_rel) ? l0 + 1 : NONE;
-            if (want != NONE) REQUEST(src, want);
+            if (c.ph != PH_DONE && pend == NONE) {          // the lines the next groups need, on their way
+                const uint32_t l0 = c.q >> LSH;
+#if SEQCDC_LW_BATCH
+                if (!has(src, l0)) want = l0;
+                else if ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) && ((l0 + 1) << LSH) < src.end_rel)
+                    want = l0 + 1;
+                if (want != NONE && !check_b(src, want & 1u)) want = NONE;   // its slot's fill still in flight
+#elif SEQCDC_LW_ONEFILL
+                // one fill site: the current line if missing, else the next once the scan is past PF
+                want = !has(src, l0) ? l0
+                       : ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) &&
+                          ((l0 + 1) << LSH) < src.end_rel) ? l0 + 1 : NONE;
+                if (want != NONE) REQUEST(src, want);
 #else
-            if (!has(src, l0)) {
-                REQUEST(src, l0);
-            } else if ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) && ((l0 + 1) << LSH) < src.end_rel) {
-                REQUEST(src, l0 + 1);
-            }
+                if (!has(src, l0)) {
+                    REQUEST(src, l0);
+                } else if ((c.q & LMASK) >= SEQCDC_LW_PF && !has(src, l0 + 1) && ((l0 + 1) << LSH) < src.end_rel) {
+                    REQUEST(src, l0 + 1);
+                }
 #endif
+            }
         }
+#if SEQCDC_LW_BATCH
+        // this step's fills: one batch barrier for the whole warp (re-armed only
+        // once its previous phase completed; if not, the lanes ask again next step)
+        if (__ballot_sync(FULL, want != NONE)) {
+            const uint32_t kb = wnext, mb = src.wb + 8 * kb, P = (wpar >> kb) & 1u;
+            uint32_t free = 1;
+            if ((wused >> kb) & 1u) {
+                if (lane == 0) free = mb_test(mb, P ^ 1u) ? 1u : 0u;
+                free = __shfl_sync(FULL, free, 0);
+            }
+            if (free) {
+                if (want != NONE) fill_b(src, want, mb, kb, P);
+                __syncwarp();                           // every async arrive counted before the phase can end
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb) : "memory");
+                wused |= 1u << kb;
+                wpar ^= 1u << kb;
+                wnext = (kb + 1) & (NBATCH - 1);
+            }
+        }
+#endif
     }
 #undef REQUEST
+#if SEQCDC_LW_BATCH
+    // every armed batch complete before the shared memory is released
+    if (lane < (int)NBATCH && ((wused >> lane) & 1u)) {
+        const uint32_t mb = src.wb + 8 * lane, P = ((wpar >> lane) & 1u) ^ 1u;
+#pragma unroll 1
+        while (!mb_test(mb, P)) {
+        }
+    }
+    __syncwarp();
+    if (lane < (int)NBATCH) mb_inval(src.wb + 8 * lane);
+#else
     drain(src);
     mb_inval(mb_of(src, 0));
     mb_inval(mb_of(src, 1));
+#endif
     {   // this warp's lanes are done and their tasks published: count them (k_lhand waits for all)
         const uint32_t mine = __popc(__ballot_sync(FULL, s < nseg));
         if (lane == 0 && mine) {
