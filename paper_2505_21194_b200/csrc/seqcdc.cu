@@ -2161,15 +2161,15 @@ SEQCDC_API const char *seqcdc_strerror(int code)
 
 SEQCDC_API const char *seqcdc_build_info(void)
 {
-    static char buf[320];
+    static char buf[512];
     int sms = 0, occ = 0, ol = 0;
     device_info(sms, occ, &ol);
     snprintf(buf, sizeof(buf),
              "seqcdc sm_100a; last call: %s walker, %u segments; warp walker: cp.async ring blk=%u nblk=%u "
-             "ahead=%u, %d/SM, win_pairs=%u; lane walker: %u-B %s lines x2 (mbarrier-polled%s), %u pairs/step "
+             "ahead=%u, %d/SM, win_pairs=%u; lane walker: %u-B %s lines x2 (mbarrier-polled%s%s), %u pairs/step "
              "(%s masks), %u-thread CTAs, %d/SM max, pf=%u; k_ext=%u",
              g_last_lane ? "lane" : "warp", g_last_nseg, BLK, NBLK, AHEAD, g_last_occ, WIN_PAIRS, lw::LINE,
-             SEQCDC_LW_BULK ? "cp.async.bulk" : "cp.async", SEQCDC_LW_LAZY ? " when needed" : " every step",
+             SEQCDC_LW_BULK ? "cp.async.bulk" : "cp.async", SEQCDC_LW_LAZY ? " when needed" : " every step", SEQCDC_LW_PAIR ? ", pair fills on misses" : "",
              lw::GRP, SEQCDC_LW_PACKED ? "packed" : "per-word", lw::THREADS, ol, (unsigned)SEQCDC_LW_PF, K_EXT);
     return buf;
 }
