@@ -77,7 +77,8 @@ def run(args, w: Workload) -> int:
 
         # end to end: each rank's pinned host shard -> device, sharded chunking, cuts -> host
         host_in = torch.empty(buf.numel(), dtype=torch.uint8, pin_memory=True)
-        host_in.copy_(buf.cpu())
+        host_in.copy_(buf)                    # device -> pinned host directly (no pageable copy of the shard)
+        torch.cuda.synchronize()
         host_cuts = torch.empty(be.out_cuts.numel(), dtype=torch.int64, pin_memory=True)
         e2e_steps = max(2, min(args.steps, 3))
         d2h = 0
